@@ -1,0 +1,427 @@
+#!/usr/bin/env python3
+"""Benchmark: fp64 SELL-32-sigma SpMV on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2|cfg1|cfg3|cfg5] [--sigma S] [--dtype f64|f32]
+
+One "step" = one SpMV y = A x over the whole matrix (all chunks), x and the
+matrix resident in HBM.  Default workload at N=1: BASELINE configs[1], the 3D
+27-point stencil on 128^3 (N=2,097,152, nnz=55,742,968), SELL-32-1, fp64.
+Its algorithmic bytes (703 MB) exceed the 126 MB L2, so no flush is needed
+between steps ("l2": "inputs larger than L2").
+
+N > 1 (torchrun, one process per GPU, NCCL): weak scaling -- the 27-point
+stencil on 128 x 128 x (128 N), row-partitioned into z-slabs of exactly the
+N=1 size, with the x halo (one 128x128 plane per neighbour) exchanged over
+NCCL and overlapped with the interior chunks (paper_1307_6209_b200/dist.py).
+
+Printed JSON (rank 0): metric/value (GF/s = 2 nnz / t, padding excluded,
+bench.py:89 of the reference), roofline of the SpMV kernel against
+MEASURED_PEAKS.json hbm_gbs, e2e through the public host-array API with
+pinned buffers, the reference CPU path timed on this host (cpu_baseline),
+clocks sampled during the timed region, and gpu_launches.
+
+``--impl reference`` times the reference's own compiled kernel core
+(oracle/_ref, built from /root/reference sources) with all host threads,
+using the reference's static schedule (spmv.py:53-58) on the same layout.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "spMVM GFLOP/s (2*nnz/t), fp64 SELL-C-sigma"
+UNIT = "GFLOP/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+
+def make_matrix(config, rank=0, world=1):
+    from paper_1307_6209_b200 import generate
+    if config == "cfg1":
+        return generate.laplace2d(1000), "2D 5-point Laplacian 1000x1000"
+    if config == "cfg2":
+        if world == 1:
+            return generate.stencil27(128), "3D 27-point stencil 128^3"
+        return None, f"3D 27-point stencil 128x128x{128 * world} (z-slabs)"
+    if config == "cfg3":
+        return generate.powerlaw(4_000_000), "power-law rows N=4M mean~20"
+    raise SystemExit(f"unknown config {config}")
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [t.strip() for t in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's compiled core (oracle/_ref) on host cores
+# ---------------------------------------------------------------------------
+
+def cpu_reference_run(o, x, budget_s=10.0, threads=None, n_chunks=None):
+    """Time the reference kernel (oracle/_ref, else the C port) with the
+    reference's static chunk split over `threads` host threads.  Returns
+    (gflops, kind, cores, sample, seconds_per_rep)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    ref = oracle.ref_kernels()
+    kind = "reference" if ref is not None else "port"
+    fn = ref.spmv_sell_range if ref is not None else oracle.spmv_sell_range
+    threads = threads or os.cpu_count() or 1
+    nch = o.n_chunks if n_chunks is None else min(n_chunks, o.n_chunks)
+    nnz = int(o.row_lengths[: nch * o.C].sum(dtype=np.int64))
+    y = np.zeros(o.n_rows_padded)
+    b = np.linspace(0, nch, threads + 1).astype(int)
+    spans = [(int(b[t]), int(b[t + 1])) for t in range(threads) if b[t + 1] > b[t]]
+    pool = ThreadPoolExecutor(max_workers=len(spans))
+
+    def one():
+        list(pool.map(lambda s: fn(o.cs, o.cl, o.C, o.col, o.val, x, y, s[0], s[1], False),
+                      spans))
+    t0 = time.perf_counter()
+    one()                                   # warm-up, also calibrates
+    t1 = max(time.perf_counter() - t0, 1e-6)
+    reps = max(1, min(1000, int(budget_s / 3 / t1)))
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            one()
+        times.append((time.perf_counter() - t0) / reps)
+    pool.shutdown()
+    best = min(times)
+    sample = (f"{nch} of {o.n_chunks} chunks ({nnz} nnz), {reps} reps x 3 trials, best trial; "
+              f"static split over {len(spans)} threads (sellkit spmv.py:53-58), "
+              f"{'oracle/_ref = reference _kernels.pyx compiled -O3' if ref else 'C port'}")
+    return 2.0 * nnz / best / 1e9, kind, len(spans), sample, best
+
+
+def host_cpu_desc():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        model = [l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")]
+        return model[0] if model else "unknown"
+    except OSError:
+        return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config == "cfg2" and world > 1:
+        from paper_1307_6209_b200 import generate
+        crs = generate.stencil27(128, nz=128 * world)
+        desc = f"3D 27-point stencil 128x128x{128 * world} (z-slabs)"
+    else:
+        crs, desc = make_matrix(args.config)
+    sigma = args.sigma
+    o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, 32, sigma)
+    x = np.random.default_rng(12345).uniform(-1, 1, crs.n_cols)
+    threads = os.cpu_count() or 1
+    # size each step so warmup + steps finish within ~2 minutes
+    gf_probe, kind, cores, _, t_full = cpu_reference_run(o, x, budget_s=1.0, threads=threads)
+    total_steps = args.steps + args.warmup
+    frac = min(1.0, 120.0 / max(total_steps * t_full, 1e-9))
+    nch = max(1, int(o.n_chunks * frac))
+    ref = oracle.ref_kernels()
+    fn = ref.spmv_sell_range if ref is not None else oracle.spmv_sell_range
+    from concurrent.futures import ThreadPoolExecutor
+    b = np.linspace(0, nch, threads + 1).astype(int)
+    spans = [(int(b[t]), int(b[t + 1])) for t in range(threads) if b[t + 1] > b[t]]
+    y = np.zeros(o.n_rows_padded)
+    nnz = int(o.row_lengths[: nch * o.C].sum(dtype=np.int64))
+    with ThreadPoolExecutor(max_workers=len(spans)) as pool:
+        def step():
+            list(pool.map(lambda s: fn(o.cs, o.cl, o.C, o.col, o.val, x, y, s[0], s[1],
+                                       False), spans))
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        dt = time.perf_counter() - t0
+    value = 2.0 * nnz * args.steps / dt / 1e9
+    sample = (f"{nch} of {o.n_chunks} chunks ({nnz} nnz) per step; static split over "
+              f"{len(spans)} threads (sellkit spmv.py:53-58); "
+              f"{'reference _kernels.pyx compiled from /root/reference sources (oracle/_ref)' if ref else 'C port (oracle/sell_oracle.c)'}; "
+              f"host {host_cpu_desc()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{desc}, SELL-32-{sigma}", "C": 32, "sigma": sigma,
+                   "n_rows": crs.n_rows, "nnz": crs.nnz},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": len(spans),
+                         "kind": "reference" if ref is not None else "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def load_profile_traffic(key):
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(key)
+    return None if v is None else float(v)
+
+
+def run_ours(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_1307_6209_b200 import dist
+        return dist.bench_main(args)
+    import oracle
+    import paper_1307_6209_b200 as sb
+    from paper_1307_6209_b200 import _lib
+    from paper_1307_6209_b200.model import algorithmic_bytes
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    crs, desc = make_matrix(args.config)
+    dt_np = np.float32 if args.dtype == "f32" else np.float64
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    sigma = args.sigma
+    x_host = np.random.default_rng(12345).uniform(-1, 1, crs.n_cols).astype(dt_np)
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = sb.crs_to_sell(crs, 32, sigma, dtype=dt_np)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    info = s.info()
+    nnz, n_pad, n_chunks, slots = info.nnz, info.n_rows_padded, info.n_chunks, info.slots
+    s_v = 4 if args.dtype == "f32" else 8
+    v_alg = algorithmic_bytes(nnz, crs.n_cols, n_pad, n_chunks, s_v=s_v)
+    lib = _lib.load()
+    handle = s.handle
+
+    xd = torch.from_numpy(x_host).to(dev)
+    yd = torch.zeros(n_pad, dtype=tdt, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    def launch():
+        _lib.check(lib.sellb_spmv(handle, xd.data_ptr(), yd.data_ptr(), 0, n_chunks, 0,
+                                  0, sp))
+
+    # parity gate on the benchmarked matrix (oracle is the checker only)
+    launch()
+    torch.cuda.synchronize()
+    parity = None
+    if not args.skip_parity:
+        o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val.astype(dt_np), crs.n_rows,
+                               crs.n_cols, 32, sigma)
+        y_ref = oracle.spmv_sell(o, x_host, threads=os.cpu_count() or 1)
+        parity = bool(yd.cpu().numpy().tobytes() == y_ref.tobytes())
+        arrays_ok = all(getattr(s, k).tobytes() == getattr(o, k).tobytes()
+                        for k in ("cs", "cl", "col", "val", "perm", "row_lengths"))
+        parity = parity and arrays_ok
+        if not parity:
+            log("PARITY FAILURE against the oracle")
+
+    for _ in range(args.warmup):
+        launch()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, per-step events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.25)
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        launch()
+        ev[i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    per = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = statistics.mean(per)
+    value = 2.0 * nnz * args.steps / (total_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peaks()
+    achieved = v_alg / (kern_ms / 1e3) / 1e9
+
+    # e2e: the public host-array API (sellb_spmv_host) with pinned x / y
+    import ctypes
+    px, py = ctypes.c_void_p(), ctypes.c_void_p()
+    _lib.check(lib.sellb_host_alloc(crs.n_cols * s_v, ctypes.byref(px)))
+    _lib.check(lib.sellb_host_alloc(n_pad * s_v, ctypes.byref(py)))
+    xh = np.ctypeslib.as_array((ctypes.c_byte * (crs.n_cols * s_v)).from_address(px.value)).view(dt_np)
+    yh = np.ctypeslib.as_array((ctypes.c_byte * (n_pad * s_v)).from_address(py.value)).view(dt_np)
+    xh[:] = x_host
+    e2e_steps = max(3, min(args.steps, 200))
+    for _ in range(3):
+        _lib.check(lib.sellb_spmv_host(handle, px.value, py.value, 0, n_chunks, 0, 0, sp))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        _lib.check(lib.sellb_spmv_host(handle, px.value, py.value, 0, n_chunks, 0, 0, sp))
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_ok = bool(yh.tobytes() == yd.cpu().numpy().tobytes())
+    lib.sellb_host_free(px)
+    lib.sellb_host_free(py)
+
+    # reference CPU path on this host, bounded sample (rank 0, N=1)
+    cpu = None
+    if not args.skip_cpu:
+        o_cpu = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, 32,
+                                   sigma)
+        gf, kind, cores, sample, _ = cpu_reference_run(o_cpu, x_host.astype(np.float64),
+                                                       budget_s=args.cpu_budget)
+        cpu = {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": sample + f"; host {host_cpu_desc()}"}
+
+    traffic = load_profile_traffic(f"{args.config}_s{sigma}_{args.dtype}")
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"{desc}, SELL-32-{sigma}", "C": 32, "sigma": sigma,
+                   "n_rows": crs.n_rows, "nnz": nnz, "slots": slots,
+                   "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
+                   "l2": "inputs larger than L2 (V_alg %.0f MB > 126 MB)" % (v_alg / 1e6)
+                   if v_alg > 126e6 else "L2-resident (V_alg < L2); no flush",
+                   "build_s": round(build_s, 4), "parity_vs_oracle": parity},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "peak_source": f"{peak_kind} hbm_gbs (copy)",
+                     "bytes_alg_per_launch": v_alg,
+                     "kernel_ms": round(kern_ms, 5)},
+        "e2e": {"value": round(2.0 * nnz / e2e_s / 1e9, 3), "unit": UNIT,
+                "h2d_bytes_per_step": crs.n_cols * s_v, "d2h_bytes_per_step": n_pad * s_v,
+                "ms_per_step": round(e2e_s * 1e3, 4), "api": "sellb_spmv_host (pinned)",
+                "matches_device": e2e_ok},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--sigma", type=int, default=1)
+    ap.add_argument("--dtype", choices=("f64", "f32"), default="f64")
+    ap.add_argument("--skip-parity", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

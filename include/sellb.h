@@ -1,0 +1,183 @@
+/*
+ * sellb.h -- C ABI of libsellb200.so, the B200-native SELL-C-sigma build and
+ * SpMV library (arXiv 1307.6209).
+ *
+ * Plain C linkage: pointers, sizes and status codes only.  Every entry point
+ * returns 0 on success or a negative status whose class mirrors the
+ * reference's exception hierarchy (/root/reference/pkg/src/sellkit/errors.py:4-25);
+ * the message is available from sellb_last_error() (thread-local).
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/sellkit):
+ *   sellb_build_from_crs      crs_to_sell                  formats.py:295-393
+ *   sellb_import              SellMatrix(...) constructor  formats.py:183-251
+ *   sellb_info                SellMatrix.nnz/stored_slots  formats.py:253-263
+ *   sellb_export              SellMatrix array fields      formats.py:201-206
+ *   sellb_spmv                spmv_sell -> spmv_sell_range spmv.py:105-122, _kernels.pyx:65-92
+ *   sellb_spmv_host           spmv_sell with host x / y    spmv.py:105-122
+ *   sellb_spmv_sell_range_host  kernels-module protocol    _kernels.pyx:65-68 (same arguments)
+ *   sellb_spmv_crs_range_host   kernels-module protocol    _kernels.pyx:17-31
+ *   sellb_spmv_crs_unrolled_range_host                     _kernels.pyx:34-62
+ *   sellb_read_sum / sellb_copy  membench kernels           _kernels.pyx:142-170
+ *   sellb_chunk_occupancy     chunk_occupancy              formats.py:274-282
+ *
+ * Threading: every entry point is safe to call concurrently from several
+ * host threads on disjoint outputs (the reference calls range kernels from a
+ * ThreadPoolExecutor, spmv.py:53-73).  Calls that take host buffers
+ * synchronise their stream before returning (blocking host-array semantics).
+ */
+#ifndef SELLB_H
+#define SELLB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.py:4-25) */
+#define SELLB_OK          0
+#define SELLB_EPARAM     -1   /* ParameterError   */
+#define SELLB_EDIM       -2   /* DimensionError   */
+#define SELLB_ESTRUCT    -3   /* StructuralError  */
+#define SELLB_ERESOURCE  -4   /* ResourceError: no device, CUDA error, OOM, NCCL */
+
+/* value types */
+#define SELLB_F64 0
+#define SELLB_F32 1
+
+/* SpMV kernel variants (sellb_set_variant) */
+#define SELLB_VARIANT_AUTO      0   /* cost model: skip padding when it saves bytes */
+#define SELLB_VARIANT_PAD_SKIP  1   /* one thread per row, stops at its row length   */
+#define SELLB_VARIANT_PAD_INCL  2   /* runs every slot up to cl (no row_lengths read) */
+
+/* output order of sellb_spmv / sellb_spmv_host */
+#define SELLB_ORDER_STORED   0      /* y[n_rows_padded] in stored (permuted) order */
+#define SELLB_ORDER_ORIGINAL 1      /* y[n_rows] in original order: fused unpermute */
+
+typedef struct sellb_mat sellb_mat;   /* opaque, library-owned, device-resident */
+
+typedef struct sellb_info_t {
+    int64_t n_rows, n_cols;
+    int64_t C, sigma, sigma_eff;
+    int64_t n_rows_padded, n_chunks;
+    int64_t slots;          /* cs[n_chunks] */
+    int64_t nnz;            /* sum(row_lengths) */
+    int32_t dtype;          /* SELLB_F64 / SELLB_F32 */
+    int32_t device;
+    int32_t col_permuted;
+    int32_t variant;        /* resolved SELLB_VARIANT_PAD_SKIP / _PAD_INCL */
+    int32_t has_row_lengths;
+    int32_t max_cl;
+} sellb_info_t;
+
+/* raw device pointers of a matrix (borrowed; valid until sellb_free) */
+typedef struct sellb_dev_arrays_t {
+    const int64_t* cs;
+    const int32_t* cl;
+    const int32_t* col;
+    const void*    val;
+    const int32_t* perm;        /* original -> stored, n_rows          */
+    const int32_t* order;       /* stored -> original, n_rows_padded    */
+    const int32_t* row_lengths; /* n_rows_padded (NULL if imported without) */
+} sellb_dev_arrays_t;
+
+const char* sellb_last_error(void);
+int sellb_version(void);
+int sellb_device_count(int32_t* n);
+
+/* ---- build / import / export -------------------------------------------- */
+
+/* crs_to_sell (formats.py:295-393) on the device.  rpt[n_rows+1], col[nnz],
+ * val[nnz] are host pointers (ptrs_on_device=0) or device pointers on
+ * `device` (ptrs_on_device=1).  Bit-exact with the reference's arrays. */
+int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val,
+                         int32_t dtype, int64_t n_rows, int64_t n_cols,
+                         int32_t C, int64_t sigma, int32_t align_bytes,
+                         int32_t permute_cols, int32_t device, void* stream,
+                         int32_t ptrs_on_device, sellb_mat** out);
+
+/* Wrap an existing SELL layout (e.g. built by the reference or read from a
+ * .sell cache).  perm / row_lengths may be NULL (row_lengths NULL => the
+ * pad-inclusive kernel, exactly the reference's loop). */
+int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col,
+                 const void* val, const int32_t* perm, const int32_t* row_lengths,
+                 int32_t dtype, int64_t n_rows, int64_t n_cols, int32_t C,
+                 int64_t sigma, int64_t n_chunks, int32_t col_permuted,
+                 int32_t device, void* stream, int32_t ptrs_on_device,
+                 sellb_mat** out);
+
+int sellb_info(const sellb_mat* m, sellb_info_t* info);
+int sellb_device_arrays(const sellb_mat* m, sellb_dev_arrays_t* out);
+
+/* Copy arrays out (host or device destination); NULL pointers are skipped. */
+int sellb_export(const sellb_mat* m, int64_t* cs, int32_t* cl, int32_t* col,
+                 void* val, int32_t* perm, int32_t* row_lengths, void* stream,
+                 int32_t ptrs_on_device);
+
+int sellb_set_variant(sellb_mat* m, int32_t variant);
+void sellb_free(sellb_mat* m);
+
+/* ---- SpMV ---------------------------------------------------------------- */
+
+/* y (+)= A x over chunks [c0, c1) on device vectors (async on `stream`).
+ * out_order STORED: y has n_rows_padded entries (reference convention,
+ * spmv.py:109-112); ORIGINAL: y has n_rows entries, written through the
+ * stored->original map (fused unpermute_vector, formats.py:433-441). */
+int sellb_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
+               int32_t accumulate, int32_t out_order, void* stream);
+
+/* Same product over a device list of chunk ids (interior/boundary split of
+ * the row-partitioned multi-GPU path). */
+int sellb_spmv_chunk_list(const sellb_mat* m, const int32_t* chunk_ids, int64_t n_ids,
+                          const void* x, void* y, int32_t accumulate, void* stream);
+
+/* End-to-end: host x[n_cols] -> device, product, device -> host y.  Blocks
+ * until y is on the host.  Pinned host buffers give full PCIe bandwidth. */
+int sellb_spmv_host(sellb_mat* m, const void* x_host, void* y_host,
+                    int64_t c0, int64_t c1, int32_t accumulate, int32_t out_order,
+                    void* stream);
+
+/* Stateless reference signature (_kernels.pyx:65-68) on HOST arrays; the
+ * extra sizes are the lengths the Python memoryviews carry implicitly. */
+int sellb_spmv_sell_range_host(const int64_t* cs, const int32_t* cl, int32_t C,
+                               const int32_t* col, const double* val, int64_t n_slots,
+                               int64_t n_chunks, const double* x, int64_t n_x,
+                               double* y, int64_t n_y, int64_t c0, int64_t c1,
+                               int32_t accumulate, int32_t device);
+
+/* CRS kernels of the same protocol (_kernels.pyx:17-62), HOST arrays. */
+int sellb_spmv_crs_range_host(const int64_t* rpt, int64_t n_rows, const int32_t* col,
+                              const double* val, int64_t nnz, const double* x,
+                              int64_t n_x, double* y, int64_t r0, int64_t r1,
+                              int32_t accumulate, int32_t unrolled, int32_t device);
+
+/* CRS kernels on device arrays. */
+int sellb_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val,
+                   int32_t dtype, const void* x, void* y, int64_t r0, int64_t r1,
+                   int32_t accumulate, int32_t unrolled, void* stream);
+
+/* ---- measurement support ------------------------------------------------- */
+
+double sellb_chunk_occupancy(const sellb_mat* m);
+/* Sector-effective occupancy: nnz / (val/col elements inside the 32-byte
+ * sectors the pad-skipping kernel touches). */
+int sellb_sector_occupancy(const sellb_mat* m, double* beta_eff, int64_t* val_sectors,
+                           int64_t* col_sectors, void* stream);
+
+/* Device read-reduce / copy bandwidth kernels (membench.py:52-116 analogs). */
+int sellb_read_sum(const double* a_dev, int64_t n, double* out_host, void* stream);
+int sellb_copy(const double* src_dev, double* dst_dev, int64_t n, void* stream);
+/* Overwrite a scratch buffer larger than L2 (timing hygiene). */
+int sellb_l2_flush(void* scratch_dev, int64_t bytes, void* stream);
+
+/* Pinned host buffers for the end-to-end path. */
+int sellb_host_alloc(size_t bytes, void** out);
+int sellb_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SELLB_H */

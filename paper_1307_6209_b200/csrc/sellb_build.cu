@@ -1,0 +1,640 @@
+// sellb_build.cu -- SELL-C-sigma construction on the device (crs_to_sell,
+// /root/reference/pkg/src/sellkit/formats.py:295-393), import / export of
+// device matrices and the kernel-variant cost model.
+//
+// Pipeline (all stream-ordered, one host sync to size val/col):
+//   1. k_row_lengths      len_pad[p] = rpt[p+1]-rpt[p] (0 for padding rows),
+//                         column-bound check, max length      (formats.py:336-338)
+//   2. k_sort_keys +      stable LSD radix sort of (scope, maxlen-len) with the
+//      cub radix sort     index as payload == np.lexsort((idx,-len,scope))
+//                                                              (formats.py:285-292)
+//   3. k_apply_order      perm[order[p]] = p, row_lengths[p] = len[order[p]]
+//                                                              (formats.py:345-349)
+//   4. k_chunk_width      cl = max over the chunk, align rounding, C*cl
+//                                                              (formats.py:351-356)
+//   5. cub scan           cs = [0, cumsum(C*cl)]               (formats.py:358-360)
+//   6. k_fill             column-major scatter with zero padding and optional
+//                         column permutation                  (formats.py:362-377)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "sellb_internal.cuh"
+
+using namespace sellb;
+
+namespace {
+
+__global__ void k_row_lengths(const int64_t* __restrict__ rpt, int64_t n, int64_t n_pad,
+                              int32_t* __restrict__ len, unsigned int* __restrict__ maxlen,
+                              int* __restrict__ bad) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned int l = 0;
+    if (p < n_pad) {
+        if (p < n) {
+            int64_t d = rpt[p + 1] - rpt[p];
+            if (d < 0 || d > 0x7fffffffLL) { atomicExch(bad, 1); d = 0; }
+            l = (unsigned int)d;
+        }
+        len[p] = (int32_t)l;
+    }
+    // warp max then one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
+    if ((threadIdx.x & 31) == 0 && l) atomicMax(maxlen, l);
+}
+
+__global__ void k_check_cols(const int32_t* __restrict__ col, int64_t nnz, int64_t n_cols,
+                             int* __restrict__ bad) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int flag = 0;
+    for (; i < nnz; i += stride) {
+        int32_t c = col[i];
+        flag |= (c < 0) | ((int64_t)c >= n_cols);
+    }
+    if (__any_sync(0xffffffffu, flag) && (threadIdx.x & 31) == 0) atomicExch(bad, 2);
+}
+
+template <typename K>
+__global__ void k_sort_keys(const int32_t* __restrict__ len, int64_t n_pad, int64_t sigma_eff,
+                            int lbits, unsigned int maxlen, K* __restrict__ keys,
+                            int32_t* __restrict__ idx) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n_pad) return;
+    K scope = (K)(p / sigma_eff);
+    K inv = (K)(maxlen - (unsigned int)len[p]);   // descending length
+    keys[p] = (scope << lbits) | inv;
+    idx[p] = (int32_t)p;
+}
+
+__global__ void k_apply_order(const int32_t* __restrict__ order, const int32_t* __restrict__ len,
+                              int64_t n, int64_t n_pad, int32_t* __restrict__ perm,
+                              int32_t* __restrict__ rl, int32_t* __restrict__ order_out) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n_pad) return;
+    int32_t o = order ? order[p] : (int32_t)p;
+    rl[p] = len[o];
+    order_out[p] = o;
+    if (o < n) perm[o] = (int32_t)p;
+}
+
+// one warp per chunk: max of the chunk's C stored-row lengths
+__global__ void k_chunk_width(const int32_t* __restrict__ rl, int64_t n_chunks, int64_t C,
+                              int64_t unit, int32_t* __restrict__ cl,
+                              int64_t* __restrict__ slots, unsigned int* __restrict__ maxcl) {
+    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (w >= n_chunks) return;
+    const int32_t* r = rl + w * C;
+    int32_t m = 0;
+    for (int64_t i = lane; i < C; i += 32) m = max(m, r[i]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+        int64_t mm = m;
+        if (unit > 1) mm = ((mm + unit - 1) / unit) * unit;
+        cl[w] = (int32_t)mm;
+        slots[w] = C * mm;
+        atomicMax(maxcl, (unsigned int)mm);
+    }
+}
+
+// one thread per stored row; consecutive threads of a chunk write consecutive
+// addresses for every slot j (coalesced stores), each thread streams its own
+// CRS row (L1-resident lines across j).
+template <typename T>
+__global__ void k_fill(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col_in,
+                       const T* __restrict__ val_in, int64_t n, int64_t n_pad, int64_t C,
+                       const int32_t* __restrict__ order, const int32_t* __restrict__ rl,
+                       const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+                       const int32_t* __restrict__ perm, int permute_cols,
+                       int32_t* __restrict__ col_out, T* __restrict__ val_out) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n_pad) return;
+    int64_t chunk = p / C;
+    int64_t dst = cs[chunk] + (p - chunk * C);
+    int32_t w = cl[chunk];
+    int32_t len = rl[p];
+    int32_t o = order[p];
+    int64_t src = (o < n) ? rpt[o] : 0;
+    for (int32_t j = 0; j < w; ++j) {
+        T v = T(0);
+        int32_t c = 0;
+        if (j < len) {
+            v = val_in[src + j];
+            c = col_in[src + j];
+            if (permute_cols) c = perm[c];
+        }
+        val_out[dst + (int64_t)j * C] = v;
+        col_out[dst + (int64_t)j * C] = c;
+    }
+}
+
+// sector accounting for the cost model: a 32-byte sector of val (4 fp64 / 8
+// fp32 lanes) or col (8 lanes) is fetched for slot j iff one of its lanes has
+// j < row length.  Sum over lane groups of the group's max length.
+__global__ void k_sector_count(const int32_t* __restrict__ rl, int64_t n_pad, int64_t C,
+                               int gv, int gc, unsigned long long* __restrict__ out) {
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // group of gc lanes
+    unsigned long long sv = 0, sc = 0;
+    int64_t p0 = g * gc;
+    if (p0 < n_pad) {
+        // groups never straddle chunks when C is a multiple of the group size;
+        // otherwise this is an estimate (documented in DESIGN.md)
+        int32_t mc = 0;
+        for (int k = 0; k < gc; k += gv) {
+            int32_t mv = 0;
+            for (int q = k; q < k + gv && p0 + q < n_pad; ++q) mv = max(mv, rl[p0 + q]);
+            sv += (unsigned long long)mv;
+            mc = max(mc, mv);
+        }
+        sc = (unsigned long long)mc;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, sv);
+        atomicAdd(out + 1, sc);
+    }
+}
+
+int64_t sigma_effective(int64_t n, int64_t C, int64_t sigma, int64_t n_pad) {
+    // formats.py:325-334
+    if (sigma <= C) return 1;
+    if (sigma >= n) return std::max<int64_t>(n_pad, 1);
+    if (sigma % C != 0) return -1;
+    return sigma;
+}
+
+int bits_for(uint64_t v) {
+    int b = 0;
+    while (b < 64 && (v >> b)) ++b;
+    return b;
+}
+
+void free_mat_arrays(sellb_mat* m) {
+    if (!m) return;
+    DeviceGuard g(m->device);
+    cudaFree(m->cs);
+    cudaFree(m->cl);
+    cudaFree(m->col);
+    cudaFree(m->val);
+    cudaFree(m->rl);
+    cudaFree(m->perm);
+    cudaFree(m->order);
+    cudaFree(m->x_buf);
+    cudaFree(m->y_buf);
+}
+
+int alloc_dev(void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return set_error(SELLB_ERESOURCE, "device allocation of %zu bytes failed: %s", bytes,
+                         cudaGetErrorString(e));
+    }
+    return 0;
+}
+
+int check_stream_error() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_error(SELLB_ERESOURCE, "kernel launch failed: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+// variant cost model: bytes of the pad-skipping kernel (touched sectors plus
+// the row_lengths stream) against the pad-inclusive one (every slot).
+int choose_variant(sellb_mat* m, cudaStream_t st, double* beta_eff_out, int64_t* vs_out,
+                   int64_t* cs_out) {
+    if (!m->rl) { m->variant = SELLB_VARIANT_PAD_INCL; return 0; }
+    if (m->n_pad == 0) { m->variant = SELLB_VARIANT_PAD_INCL; return 0; }
+    DBuf cnt;
+    SELLB_CU(cnt.alloc(2 * sizeof(unsigned long long), st));
+    SELLB_CU(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), st));
+    int gv = m->dtype == SELLB_F32 ? 8 : 4, gc = 8;
+    int64_t groups = (m->n_pad + gc - 1) / gc;
+    k_sector_count<<<(unsigned)grid_for(groups, 256), 256, 0, st>>>(
+        m->rl, m->n_pad, m->C, gv, gc, cnt.as<unsigned long long>());
+    if (int rc = check_stream_error()) return rc;
+    unsigned long long h[2];
+    SELLB_CU(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    double sv = (double)vsize(m->dtype);
+    double bytes_skip = 32.0 * (double)h[0] + 32.0 * (double)h[1] + 4.0 * (double)m->n_pad;
+    double bytes_incl = (sv + 4.0) * (double)m->slots;
+    if (vs_out) *vs_out = (int64_t)h[0];
+    if (cs_out) *cs_out = (int64_t)h[1];
+    if (beta_eff_out) {
+        double touched = 32.0 * (double)h[0] + 32.0 * (double)h[1];
+        *beta_eff_out = touched > 0 ? (sv + 4.0) * (double)m->nnz / touched : 1.0;
+    }
+    if (m->variant == SELLB_VARIANT_AUTO || m->variant == 0)
+        m->variant = bytes_skip < bytes_incl ? SELLB_VARIANT_PAD_SKIP : SELLB_VARIANT_PAD_INCL;
+    return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// ABI
+// ===========================================================================
+extern "C" {
+
+int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val, int32_t dtype,
+                         int64_t n_rows, int64_t n_cols, int32_t C, int64_t sigma,
+                         int32_t align_bytes, int32_t permute_cols, int32_t device, void* stream,
+                         int32_t ptrs_on_device, sellb_mat** out) {
+    clear_error();
+    if (!out) return set_error(SELLB_EPARAM, "out must not be NULL");
+    *out = nullptr;
+    // parameter checks in the reference's order (formats.py:309-319)
+    if (C < 1) return set_error(SELLB_EPARAM, "chunk height C must be >= 1, got %d", C);
+    if (sigma < 1) return set_error(SELLB_EPARAM, "sigma must be >= 1, got %lld", (long long)sigma);
+    if (align_bytes != 1 && align_bytes != 64)
+        return set_error(SELLB_EPARAM, "align_bytes must be 1 or 64, got %d", align_bytes);
+    if (permute_cols && n_rows != n_cols)
+        return set_error(SELLB_EPARAM,
+                         "column permutation requires a square matrix (got %lldx%lld); rows "
+                         "and columns share one index space",
+                         (long long)n_rows, (long long)n_cols);
+    if (dtype != SELLB_F64 && dtype != SELLB_F32)
+        return set_error(SELLB_EPARAM, "dtype must be SELLB_F64 or SELLB_F32");
+    if (n_rows < 0 || n_cols < 0)
+        return set_error(SELLB_ESTRUCT, "negative matrix dimension (%lldx%lld)", (long long)n_rows,
+                         (long long)n_cols);
+    if (n_rows >= (1LL << 31) || n_cols >= (1LL << 31))
+        return set_error(SELLB_ESTRUCT, "matrix dimension exceeds 4-byte index range");
+    if (!rpt) return set_error(SELLB_EPARAM, "rpt must not be NULL");
+
+    const int64_t n = n_rows;
+    const int64_t n_pad = n ? ((n + C - 1) / C) * C : 0;
+    const int64_t n_chunks = n_pad / C;
+    if (n_pad >= (1LL << 31)) return set_error(SELLB_ESTRUCT, "padded row count exceeds int32");
+    const int64_t sigma_eff = sigma_effective(n, C, sigma, n_pad);
+    if (sigma_eff < 0)
+        return set_error(SELLB_EPARAM,
+                         "sigma (%lld) must be a multiple of C (%d) when C < sigma < n_rows",
+                         (long long)sigma, C);
+
+    DeviceGuard guard(device);
+    if (!guard.ok) return set_error(SELLB_ERESOURCE, "cannot select CUDA device %d", device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t vs = vsize(dtype);
+
+    // --- inputs on device -------------------------------------------------
+    int64_t rpt_host_last = 0, rpt_host_first = 0;
+    if (ptrs_on_device) {
+        SELLB_CU(cudaMemcpyAsync(&rpt_host_first, rpt, 8, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaMemcpyAsync(&rpt_host_last, rpt + n, 8, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+    } else {
+        rpt_host_first = rpt[0];
+        rpt_host_last = rpt[n];
+    }
+    if (n && rpt_host_first != 0) return set_error(SELLB_ESTRUCT, "rpt[0] must be 0");
+    const int64_t nnz = rpt_host_last;
+    if (nnz < 0) return set_error(SELLB_ESTRUCT, "rpt[-1] must be >= 0");
+    if (nnz && (!col || !val)) return set_error(SELLB_EPARAM, "col/val must not be NULL");
+
+    DBuf d_rpt, d_col, d_val;
+    const int64_t* rpt_d = rpt;
+    const int32_t* col_d = col;
+    const void* val_d = val;
+    if (!ptrs_on_device) {
+        SELLB_CU(d_rpt.alloc((n + 1) * 8, st));
+        SELLB_CU(cudaMemcpyAsync(d_rpt.p, rpt, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+        SELLB_CU(d_col.alloc(nnz * 4, st));
+        SELLB_CU(d_val.alloc(nnz * vs, st));
+        if (nnz) {
+            SELLB_CU(cudaMemcpyAsync(d_col.p, col, nnz * 4, cudaMemcpyHostToDevice, st));
+            SELLB_CU(cudaMemcpyAsync(d_val.p, val, nnz * vs, cudaMemcpyHostToDevice, st));
+        }
+        rpt_d = d_rpt.as<int64_t>();
+        col_d = d_col.as<int32_t>();
+        val_d = d_val.p;
+    }
+
+    sellb_mat* m = new (std::nothrow) sellb_mat();
+    if (!m) return set_error(SELLB_ERESOURCE, "host allocation failed");
+    struct Holder {
+        sellb_mat* m;
+        ~Holder() { if (m) { free_mat_arrays(m); delete m; } }
+    } holder{m};
+    m->n_rows = n; m->n_cols = n_cols; m->C = C; m->sigma = sigma; m->sigma_eff = sigma_eff;
+    m->n_pad = n_pad; m->n_chunks = n_chunks; m->nnz = nnz; m->dtype = dtype;
+    m->device = device; m->col_permuted = permute_cols ? 1 : 0;
+    m->variant = SELLB_VARIANT_AUTO;
+
+    // --- 1. lengths + checks ------------------------------------------------
+    DBuf d_len, d_flags;
+    SELLB_CU(d_len.alloc(n_pad * 4, st));
+    SELLB_CU(d_flags.alloc(16, st));
+    SELLB_CU(cudaMemsetAsync(d_flags.p, 0, 16, st));
+    unsigned int* d_maxlen = d_flags.as<unsigned int>();
+    int* d_bad = reinterpret_cast<int*>(d_flags.as<unsigned int>() + 1);
+    unsigned int* d_maxcl = d_flags.as<unsigned int>() + 2;
+    if (n_pad)
+        k_row_lengths<<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(rpt_d, n, n_pad,
+                                                                       d_len.as<int32_t>(),
+                                                                       d_maxlen, d_bad);
+    if (nnz) {
+        int blocks = (int)std::min<int64_t>(grid_for(nnz, 256), 148 * 16);
+        k_check_cols<<<blocks, 256, 0, st>>>(col_d, nnz, n_cols, d_bad);
+    }
+    if (int rc = check_stream_error()) return rc;
+    unsigned int hflags[2] = {0, 0};
+    SELLB_CU(cudaMemcpyAsync(hflags, d_flags.p, 8, cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    if (hflags[1] == 1) return set_error(SELLB_ESTRUCT, "rpt must be non-decreasing");
+    if (hflags[1] == 2) return set_error(SELLB_ESTRUCT, "column index out of bounds");
+    const unsigned int maxlen = hflags[0];
+
+    // --- 2. scope sort --------------------------------------------------------
+    if (int rc = alloc_dev((void**)&m->perm, std::max<int64_t>(n, 1) * 4)) return rc;
+    if (int rc = alloc_dev((void**)&m->rl, std::max<int64_t>(n_pad, 1) * 4)) return rc;
+    if (int rc = alloc_dev((void**)&m->order, std::max<int64_t>(n_pad, 1) * 4)) return rc;
+    DBuf d_sorted_idx;
+    const int32_t* order_in = nullptr;
+    if (sigma_eff > 1 && n_pad > 1) {
+        const int lbits = std::max(1, bits_for(maxlen));
+        const int64_t n_scopes = (n_pad + sigma_eff - 1) / sigma_eff;
+        const int sbits = n_scopes > 1 ? bits_for((uint64_t)(n_scopes - 1)) : 0;
+        const int total_bits = lbits + sbits;
+        DBuf d_idx_in, d_keys_in, d_keys_out, d_tmp;
+        SELLB_CU(d_idx_in.alloc(n_pad * 4, st));
+        SELLB_CU(d_sorted_idx.alloc(n_pad * 4, st));
+        size_t tmp_bytes = 0;
+        if (total_bits <= 32) {
+            SELLB_CU(d_keys_in.alloc(n_pad * 4, st));
+            SELLB_CU(d_keys_out.alloc(n_pad * 4, st));
+            k_sort_keys<uint32_t><<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
+                d_len.as<int32_t>(), n_pad, sigma_eff, lbits, maxlen, d_keys_in.as<uint32_t>(),
+                d_idx_in.as<int32_t>());
+            SELLB_CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_keys_in.as<uint32_t>(),
+                                                     d_keys_out.as<uint32_t>(),
+                                                     d_idx_in.as<int32_t>(),
+                                                     d_sorted_idx.as<int32_t>(), (int)n_pad, 0,
+                                                     total_bits, st));
+            SELLB_CU(d_tmp.alloc(tmp_bytes, st));
+            SELLB_CU(cub::DeviceRadixSort::SortPairs(d_tmp.p, tmp_bytes, d_keys_in.as<uint32_t>(),
+                                                     d_keys_out.as<uint32_t>(),
+                                                     d_idx_in.as<int32_t>(),
+                                                     d_sorted_idx.as<int32_t>(), (int)n_pad, 0,
+                                                     total_bits, st));
+        } else {
+            SELLB_CU(d_keys_in.alloc(n_pad * 8, st));
+            SELLB_CU(d_keys_out.alloc(n_pad * 8, st));
+            k_sort_keys<uint64_t><<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
+                d_len.as<int32_t>(), n_pad, sigma_eff, lbits, maxlen, d_keys_in.as<uint64_t>(),
+                d_idx_in.as<int32_t>());
+            SELLB_CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_keys_in.as<uint64_t>(),
+                                                     d_keys_out.as<uint64_t>(),
+                                                     d_idx_in.as<int32_t>(),
+                                                     d_sorted_idx.as<int32_t>(), (int)n_pad, 0,
+                                                     total_bits, st));
+            SELLB_CU(d_tmp.alloc(tmp_bytes, st));
+            SELLB_CU(cub::DeviceRadixSort::SortPairs(d_tmp.p, tmp_bytes, d_keys_in.as<uint64_t>(),
+                                                     d_keys_out.as<uint64_t>(),
+                                                     d_idx_in.as<int32_t>(),
+                                                     d_sorted_idx.as<int32_t>(), (int)n_pad, 0,
+                                                     total_bits, st));
+        }
+        order_in = d_sorted_idx.as<int32_t>();
+    }
+    // --- 3. perm / row_lengths / order ------------------------------------------
+    if (n_pad)
+        k_apply_order<<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
+            order_in, d_len.as<int32_t>(), n, n_pad, m->perm, m->rl, m->order);
+
+    // --- 4. chunk widths + 5. cs ----------------------------------------------
+    if (int rc = alloc_dev((void**)&m->cl, std::max<int64_t>(n_chunks, 1) * 4)) return rc;
+    if (int rc = alloc_dev((void**)&m->cs, (n_chunks + 1) * 8)) return rc;
+    SELLB_CU(cudaMemsetAsync(m->cs, 0, 8, st));
+    int64_t unit = 1;
+    if (align_bytes > 1) {
+        int64_t a = 4LL * C, b = align_bytes;
+        while (b) { int64_t t = a % b; a = b; b = t; }
+        unit = align_bytes / a;   // formats.py:354
+    }
+    if (n_chunks) {
+        DBuf d_slots, d_tmp;
+        SELLB_CU(d_slots.alloc(n_chunks * 8, st));
+        k_chunk_width<<<(unsigned)grid_for(n_chunks * 32, 256), 256, 0, st>>>(
+            m->rl, n_chunks, C, unit, m->cl, d_slots.as<int64_t>(), d_maxcl);
+        size_t tmp_bytes = 0;
+        SELLB_CU(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_slots.as<int64_t>(),
+                                               m->cs + 1, (int)n_chunks, st));
+        SELLB_CU(d_tmp.alloc(tmp_bytes, st));
+        SELLB_CU(cub::DeviceScan::InclusiveSum(d_tmp.p, tmp_bytes, d_slots.as<int64_t>(),
+                                               m->cs + 1, (int)n_chunks, st));
+    }
+    if (int rc = check_stream_error()) return rc;
+    int64_t total = 0;
+    unsigned int maxcl = 0;
+    SELLB_CU(cudaMemcpyAsync(&total, m->cs + n_chunks, 8, cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaMemcpyAsync(&maxcl, d_maxcl, 4, cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    m->slots = total;
+    m->max_cl = (int32_t)maxcl;
+
+    // --- 6. fill -------------------------------------------------------------
+    if (int rc = alloc_dev((void**)&m->col, total * 4)) return rc;
+    if (int rc = alloc_dev(&m->val, total * vs)) return rc;
+    if (n_pad && total) {
+        if (dtype == SELLB_F64)
+            k_fill<double><<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
+                rpt_d, col_d, (const double*)val_d, n, n_pad, C, m->order, m->rl, m->cs, m->cl,
+                m->perm, permute_cols ? 1 : 0, m->col, (double*)m->val);
+        else
+            k_fill<float><<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
+                rpt_d, col_d, (const float*)val_d, n, n_pad, C, m->order, m->rl, m->cs, m->cl,
+                m->perm, permute_cols ? 1 : 0, m->col, (float*)m->val);
+    }
+    if (int rc = check_stream_error()) return rc;
+    if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
+    SELLB_CU(cudaStreamSynchronize(st));
+    holder.m = nullptr;
+    *out = m;
+    return 0;
+}
+
+int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const void* val,
+                 const int32_t* perm, const int32_t* row_lengths, int32_t dtype, int64_t n_rows,
+                 int64_t n_cols, int32_t C, int64_t sigma, int64_t n_chunks, int32_t col_permuted,
+                 int32_t device, void* stream, int32_t ptrs_on_device, sellb_mat** out) {
+    clear_error();
+    if (!out) return set_error(SELLB_EPARAM, "out must not be NULL");
+    *out = nullptr;
+    if (C < 1) return set_error(SELLB_EPARAM, "chunk height C must be >= 1, got %d", C);
+    if (dtype != SELLB_F64 && dtype != SELLB_F32)
+        return set_error(SELLB_EPARAM, "dtype must be SELLB_F64 or SELLB_F32");
+    if (n_rows < 0 || n_cols < 0 || n_chunks < 0)
+        return set_error(SELLB_ESTRUCT, "negative dimension");
+    if (n_chunks * (int64_t)C < n_rows || (n_rows && n_chunks * (int64_t)C >= n_rows + C))
+        return set_error(SELLB_ESTRUCT, "n_rows_padded must be n_rows rounded up to C");
+    if (!cs || (n_chunks && !cl)) return set_error(SELLB_EPARAM, "cs/cl must not be NULL");
+    DeviceGuard guard(device);
+    if (!guard.ok) return set_error(SELLB_ERESOURCE, "cannot select CUDA device %d", device);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemcpyKind kind = ptrs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    int64_t total = 0;
+    if (ptrs_on_device) {
+        SELLB_CU(cudaMemcpyAsync(&total, cs + n_chunks, 8, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+    } else {
+        total = cs[n_chunks];
+    }
+    if (total < 0) return set_error(SELLB_ESTRUCT, "cs[n_chunks] must be >= 0");
+    if (total && (!col || !val)) return set_error(SELLB_EPARAM, "col/val must not be NULL");
+    sellb_mat* m = new (std::nothrow) sellb_mat();
+    if (!m) return set_error(SELLB_ERESOURCE, "host allocation failed");
+    struct Holder {
+        sellb_mat* m;
+        ~Holder() { if (m) { free_mat_arrays(m); delete m; } }
+    } holder{m};
+    const size_t vs = vsize(dtype);
+    m->n_rows = n_rows; m->n_cols = n_cols; m->C = C; m->sigma = sigma;
+    m->n_pad = n_chunks * C; m->n_chunks = n_chunks; m->slots = total; m->dtype = dtype;
+    m->device = device; m->col_permuted = col_permuted;
+    m->sigma_eff = sigma_effective(n_rows, C, sigma, m->n_pad);
+    if (int rc = alloc_dev((void**)&m->cs, (n_chunks + 1) * 8)) return rc;
+    if (int rc = alloc_dev((void**)&m->cl, std::max<int64_t>(n_chunks, 1) * 4)) return rc;
+    if (int rc = alloc_dev((void**)&m->col, total * 4)) return rc;
+    if (int rc = alloc_dev(&m->val, total * vs)) return rc;
+    SELLB_CU(cudaMemcpyAsync(m->cs, cs, (n_chunks + 1) * 8, kind, st));
+    if (n_chunks) SELLB_CU(cudaMemcpyAsync(m->cl, cl, n_chunks * 4, kind, st));
+    if (total) {
+        SELLB_CU(cudaMemcpyAsync(m->col, col, total * 4, kind, st));
+        SELLB_CU(cudaMemcpyAsync(m->val, val, total * vs, kind, st));
+    }
+    if (perm && n_rows) {
+        if (int rc = alloc_dev((void**)&m->perm, n_rows * 4)) return rc;
+        SELLB_CU(cudaMemcpyAsync(m->perm, perm, n_rows * 4, kind, st));
+        // stored -> original map for the fused unpermute epilogue
+        if (int rc = alloc_dev((void**)&m->order, std::max<int64_t>(m->n_pad, 1) * 4)) return rc;
+        std::vector<int32_t> h_perm(n_rows), h_order(m->n_pad);
+        SELLB_CU(cudaMemcpyAsync(h_perm.data(), m->perm, n_rows * 4, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+        for (int64_t p = 0; p < m->n_pad; ++p) h_order[p] = (int32_t)p;   // padding rows
+        for (int64_t i = 0; i < n_rows; ++i) {
+            int32_t p = h_perm[i];
+            if (p < 0 || p >= n_rows) return set_error(SELLB_ESTRUCT, "perm must be a permutation");
+            h_order[p] = (int32_t)i;
+        }
+        SELLB_CU(cudaMemcpyAsync(m->order, h_order.data(), m->n_pad * 4, cudaMemcpyHostToDevice, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+    }
+    // max cl
+    if (n_chunks) {
+        std::vector<int32_t> h_cl(n_chunks);
+        SELLB_CU(cudaMemcpyAsync(h_cl.data(), m->cl, n_chunks * 4, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+        int32_t mx = 0;
+        for (auto v : h_cl) mx = std::max(mx, v);
+        m->max_cl = mx;
+    }
+    if (row_lengths && m->n_pad) {
+        if (int rc = alloc_dev((void**)&m->rl, m->n_pad * 4)) return rc;
+        SELLB_CU(cudaMemcpyAsync(m->rl, row_lengths, m->n_pad * 4, kind, st));
+        std::vector<int32_t> h_rl(m->n_pad);
+        SELLB_CU(cudaMemcpyAsync(h_rl.data(), m->rl, m->n_pad * 4, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+        int64_t s = 0;
+        for (auto v : h_rl) s += v;
+        m->nnz = s;
+        m->variant = SELLB_VARIANT_AUTO;
+        if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
+    } else {
+        m->nnz = -1;   // unknown without row_lengths
+        m->variant = SELLB_VARIANT_PAD_INCL;
+    }
+    SELLB_CU(cudaStreamSynchronize(st));
+    holder.m = nullptr;
+    *out = m;
+    return 0;
+}
+
+int sellb_info(const sellb_mat* m, sellb_info_t* info) {
+    clear_error();
+    if (!m || !info) return set_error(SELLB_EPARAM, "NULL argument");
+    info->n_rows = m->n_rows; info->n_cols = m->n_cols; info->C = m->C; info->sigma = m->sigma;
+    info->sigma_eff = m->sigma_eff; info->n_rows_padded = m->n_pad; info->n_chunks = m->n_chunks;
+    info->slots = m->slots; info->nnz = m->nnz; info->dtype = m->dtype; info->device = m->device;
+    info->col_permuted = m->col_permuted; info->variant = m->variant;
+    info->has_row_lengths = m->rl != nullptr; info->max_cl = m->max_cl;
+    return 0;
+}
+
+int sellb_device_arrays(const sellb_mat* m, sellb_dev_arrays_t* o) {
+    clear_error();
+    if (!m || !o) return set_error(SELLB_EPARAM, "NULL argument");
+    o->cs = m->cs; o->cl = m->cl; o->col = m->col; o->val = m->val; o->perm = m->perm;
+    o->order = m->order; o->row_lengths = m->rl;
+    return 0;
+}
+
+int sellb_export(const sellb_mat* m, int64_t* cs, int32_t* cl, int32_t* col, void* val,
+                 int32_t* perm, int32_t* row_lengths, void* stream, int32_t ptrs_on_device) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    DeviceGuard guard(m->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemcpyKind kind = ptrs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (cs) SELLB_CU(cudaMemcpyAsync(cs, m->cs, (m->n_chunks + 1) * 8, kind, st));
+    if (cl && m->n_chunks) SELLB_CU(cudaMemcpyAsync(cl, m->cl, m->n_chunks * 4, kind, st));
+    if (col && m->slots) SELLB_CU(cudaMemcpyAsync(col, m->col, m->slots * 4, kind, st));
+    if (val && m->slots) SELLB_CU(cudaMemcpyAsync(val, m->val, m->slots * vsize(m->dtype), kind, st));
+    if (perm && m->n_rows) {
+        if (!m->perm) return set_error(SELLB_EPARAM, "matrix has no permutation");
+        SELLB_CU(cudaMemcpyAsync(perm, m->perm, m->n_rows * 4, kind, st));
+    }
+    if (row_lengths && m->n_pad) {
+        if (!m->rl) return set_error(SELLB_EPARAM, "matrix has no row_lengths");
+        SELLB_CU(cudaMemcpyAsync(row_lengths, m->rl, m->n_pad * 4, kind, st));
+    }
+    SELLB_CU(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int sellb_set_variant(sellb_mat* m, int32_t variant) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    if (variant < SELLB_VARIANT_AUTO || variant > SELLB_VARIANT_PAD_INCL)
+        return set_error(SELLB_EPARAM, "unknown variant %d", variant);
+    if (variant == SELLB_VARIANT_PAD_SKIP && !m->rl)
+        return set_error(SELLB_EPARAM, "pad-skipping needs row_lengths");
+    DeviceGuard guard(m->device);
+    m->variant = variant;
+    if (variant == SELLB_VARIANT_AUTO) return choose_variant(m, 0, nullptr, nullptr, nullptr);
+    return 0;
+}
+
+void sellb_free(sellb_mat* m) {
+    if (!m) return;
+    free_mat_arrays(m);
+    delete m;
+}
+
+double sellb_chunk_occupancy(const sellb_mat* m) {
+    // formats.py:274-282
+    if (!m || m->slots == 0) return 1.0;
+    return (double)m->nnz / (double)m->slots;
+}
+
+int sellb_sector_occupancy(const sellb_mat* m, double* beta_eff, int64_t* val_sectors,
+                           int64_t* col_sectors, void* stream) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    if (!m->rl) return set_error(SELLB_EPARAM, "matrix has no row_lengths");
+    DeviceGuard guard(m->device);
+    sellb_mat* mm = const_cast<sellb_mat*>(m);
+    int32_t keep = mm->variant;
+    int rc = choose_variant(mm, (cudaStream_t)stream, beta_eff, val_sectors, col_sectors);
+    mm->variant = keep;
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// sellb_internal.cuh -- shared internals of libsellb200.so (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/sellb.h"
+
+// ---------------------------------------------------------------------------
+// Device-resident SELL-C-sigma matrix.
+//
+// HBM layout (one cudaMalloc per array, 256-byte aligned by the allocator):
+//   cs   int64[n_chunks+1]   chunk start offsets (formats.py:358-360)
+//   cl   int32[n_chunks]     chunk widths, align-rounded (formats.py:351-356)
+//   col  int32[slots]        column-major chunk storage, padding = 0
+//   val  T[slots]            T = double | float, padding = 0.0
+//   rl   int32[n_pad]        stored-row lengths (row_lengths)
+//   perm int32[n_rows]       original -> stored
+//   order int32[n_pad]       stored -> original (>= n_rows for padding rows)
+// Element (stored row p, slot j) lives at cs[p / C] + j*C + p % C
+// (formats.py:185-193), so for C = 32 one warp reads 32 consecutive values
+// (256 B fp64) and 32 consecutive indices (128 B) per slot: fully coalesced.
+// ---------------------------------------------------------------------------
+struct sellb_mat {
+    int64_t n_rows = 0, n_cols = 0, C = 1, sigma = 1, sigma_eff = 1;
+    int64_t n_pad = 0, n_chunks = 0, slots = 0, nnz = 0;
+    int32_t dtype = SELLB_F64, device = 0, col_permuted = 0;
+    int32_t variant = SELLB_VARIANT_PAD_INCL, max_cl = 0;
+    int64_t* cs = nullptr;
+    int32_t* cl = nullptr;
+    int32_t* col = nullptr;
+    void* val = nullptr;
+    int32_t* rl = nullptr;
+    int32_t* perm = nullptr;
+    int32_t* order = nullptr;
+    // end-to-end staging (device x / y for sellb_spmv_host)
+    void* x_buf = nullptr;
+    void* y_buf = nullptr;
+    std::mutex mu;
+};
+
+namespace sellb {
+
+int set_error(int code, const char* fmt, ...);
+void clear_error();
+
+inline size_t vsize(int32_t dtype) { return dtype == SELLB_F32 ? 4 : 8; }
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// RAII device buffer (stream-ordered free)
+struct DBuf {
+    void* p = nullptr;
+    cudaStream_t s = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { if (p) cudaFreeAsync(p, s); }
+    cudaError_t alloc(size_t bytes, cudaStream_t st) {
+        s = st;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+    }
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+    void* release() { void* q = p; p = nullptr; return q; }
+};
+
+// launch helpers implemented in sellb_spmv.cu
+int launch_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
+                int accumulate, int out_order, cudaStream_t st);
+int launch_spmv_list(const sellb_mat* m, const int32_t* ids, int64_t n_ids, const void* x,
+                     void* y, int accumulate, cudaStream_t st);
+int launch_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val, int32_t dtype,
+                    const void* x, void* y, int64_t r0, int64_t r1, int accumulate,
+                    int unrolled, cudaStream_t st);
+
+inline int64_t grid_for(int64_t n, int threads) { return (n + threads - 1) / threads; }
+
+}  // namespace sellb
+
+#define SELLB_CU(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return sellb::set_error(SELLB_ERESOURCE, "%s failed: %s (%s:%d)", #call,   \
+                                    cudaGetErrorString(e_), __FILE__, __LINE__);        \
+    } while (0)

@@ -1,0 +1,440 @@
+// sellb_spmv.cu -- SELL-C-sigma SpMV kernels for sm_100a.
+//
+// The reference kernel (/root/reference/pkg/src/sellkit/_kernels.pyx:65-92):
+//   for each chunk i: tmp[r] = 0 for r < C
+//     for j < cl[i]: for r < C: tmp[r] = tmp[r] + val[cs[i]+j*C+r] * x[col[...]]
+//     y[i*C+r] = tmp[r]            (or y = y + tmp when accumulating)
+//
+// B200 mapping: one thread per stored row (the paper's GPU design,
+// PAPER.md:770-779, :995-998).  For C = 32 a warp owns a chunk, so each slot j
+// is one fully coalesced 256 B (fp64) value load and one 128 B index load.
+// The RHS x is gathered through the read-only path (ld.global.nc), matrix
+// streams are marked L1::no_allocate with an L2 evict-first policy so they do
+// not push x out of the 126 MB L2.
+//
+// Bitwise parity with the reference: each row is summed by exactly one thread,
+// from +0.0, in ascending slot order, with separately rounded multiply and
+// add (__dmul_rn / __dadd_rn: no FMA contraction; the compiled reference has
+// none either).  Loads are batched U slots at a time for memory-level
+// parallelism, but the adds are issued in slot order.
+//
+// Padding: the PAD_SKIP variant stops each thread at its own row length (the
+// paper's "Sliced ELLR-T, T=1" optimisation).  The reference adds
+// 0.0 * x[0] for every padded slot; for finite x[0] that is an exact no-op
+// (the running sum starts at +0.0 and can never become -0.0), and for
+// non-finite x[0] it turns the row into NaN.  One fused fix-up
+// (sum += 0 * x[0] when the row has padding) reproduces that exactly, so both
+// variants are bit-identical to the reference for every input.
+#include <algorithm>
+
+#include "sellb_internal.cuh"
+
+using namespace sellb;
+
+namespace {
+
+template <typename T> struct Arith;
+template <> struct Arith<double> {
+    __device__ static __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    __device__ static __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+};
+template <> struct Arith<float> {
+    __device__ static __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+    __device__ static __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+};
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// streaming (read-once) loads of the matrix arrays
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p, uint64_t pol) {
+    float v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
+    int32_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// RHS gather: read-only path, keep in L2
+__device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_x(const float* p, uint64_t pol) {
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+constexpr int kThreads = 256;
+
+// One thread per stored row p in [p0, p1).  CC > 0: compile-time chunk height.
+// ORD 0: y[p] in stored order; ORD 1: y[order[p]] for real rows (fused unpermute).
+template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U>
+__global__ void __launch_bounds__(kThreads)
+k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+            const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+            const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+            const int32_t* __restrict__ order, int64_t C_rt, int64_t p0, int64_t p1,
+            int64_t n_rows) {
+    const int64_t C = CC > 0 ? (int64_t)CC : C_rt;
+    const int64_t p = p0 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (p >= p1) return;
+    const int64_t chunk = p / C;
+    const int64_t base = cs[chunk] + (p - chunk * C);
+    const int w = cl[chunk];
+    const int len = SKIP ? rl[p] : w;
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const T* vp = val + base;
+    const int32_t* cp = col + base;
+    T sum = T(0);
+    int j = 0;
+    for (; j + U <= len; j += U) {
+        T v[U];
+        int32_t c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            v[u] = ld_stream(vp + (int64_t)(j + u) * C, pol_s);
+            c[u] = ld_stream(cp + (int64_t)(j + u) * C, pol_s);
+        }
+        T xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u], pol_x);
+#pragma unroll
+        for (int u = 0; u < U; ++u) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
+    }
+    if (j < len) {   // predicated tail batch
+        T v[U];
+        int32_t c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (j + u < len) {
+                v[u] = ld_stream(vp + (int64_t)(j + u) * C, pol_s);
+                c[u] = ld_stream(cp + (int64_t)(j + u) * C, pol_s);
+            } else {
+                v[u] = T(0);
+                c[u] = 0;
+            }
+        }
+        T xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = (j + u < len) ? ld_x(x + c[u], pol_x) : T(0);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (j + u < len) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
+    }
+    if (SKIP && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+    if (ORD == 0) {
+        T out = ACC ? Arith<T>::add(y[p], sum) : sum;
+        __stcs(y + p, out);
+    } else if (p < n_rows) {
+        const int64_t o = order[p];
+        T out = ACC ? Arith<T>::add(y[o], sum) : sum;
+        y[o] = out;
+    }
+}
+
+// Chunk-list variant (multi-GPU interior / boundary passes): block b handles
+// kThreads consecutive stored rows of chunk ids[...]; generic C.
+template <typename T, bool SKIP, bool ACC>
+__global__ void __launch_bounds__(kThreads)
+k_spmv_sell_list(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+                 const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+                 const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+                 const int32_t* __restrict__ ids, int64_t n_ids, int64_t C) {
+    const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (t >= n_ids * C) return;
+    const int64_t k = t / C;
+    const int64_t r = t - k * C;
+    const int64_t chunk = ids[k];
+    const int64_t p = chunk * C + r;
+    const int64_t base = cs[chunk] + r;
+    const int w = cl[chunk];
+    const int len = SKIP ? rl[p] : w;
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    T sum = T(0);
+    for (int j = 0; j < len; ++j) {
+        T v = ld_stream(val + base + (int64_t)j * C, pol_s);
+        int32_t c = ld_stream(col + base + (int64_t)j * C, pol_s);
+        sum = Arith<T>::add(sum, Arith<T>::mul(v, ld_x(x + c, pol_x)));
+    }
+    if (SKIP && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+    y[p] = ACC ? Arith<T>::add(y[p], sum) : sum;
+}
+
+// CRS kernels (_kernels.pyx:17-62), one thread per row, reference order.
+template <typename T, bool ACC>
+__global__ void __launch_bounds__(kThreads)
+k_spmv_crs(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
+           const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y, int64_t r0,
+           int64_t r1) {
+    const int64_t i = r0 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (i >= r1) return;
+    T tmp = T(0);
+    for (int64_t j = rpt[i]; j < rpt[i + 1]; ++j)
+        tmp = Arith<T>::add(tmp, Arith<T>::mul(val[j], __ldg(x + col[j])));
+    y[i] = ACC ? Arith<T>::add(y[i], tmp) : tmp;
+}
+
+template <typename T, bool ACC>
+__global__ void __launch_bounds__(kThreads)
+k_spmv_crs_unrolled(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
+                    const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+                    int64_t r0, int64_t r1) {
+    using A = Arith<T>;
+    const int64_t i = r0 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (i >= r1) return;
+    const int64_t s = rpt[i], e = rpt[i + 1];
+    const int64_t m = s + ((e - s) & ~(int64_t)3);
+    T t0 = 0, t1 = 0, t2 = 0, t3 = 0, acc;
+    int64_t j = s;
+    for (; j < m; j += 4) {
+        t0 = A::add(t0, A::mul(val[j], __ldg(x + col[j])));
+        t1 = A::add(t1, A::mul(val[j + 1], __ldg(x + col[j + 1])));
+        t2 = A::add(t2, A::mul(val[j + 2], __ldg(x + col[j + 2])));
+        t3 = A::add(t3, A::mul(val[j + 3], __ldg(x + col[j + 3])));
+    }
+    const T comb = A::add(A::add(A::add(t0, t1), t2), t3);
+    acc = ACC ? A::add(y[i], comb) : comb;
+    for (; j < e; ++j) acc = A::add(acc, A::mul(val[j], __ldg(x + col[j])));
+    y[i] = acc;
+}
+
+template <typename T, int CC, bool SKIP, bool ACC, int ORD>
+int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1,
+               cudaStream_t st) {
+    const int64_t rows = p1 - p0;
+    if (rows <= 0) return 0;
+    const unsigned grid = (unsigned)grid_for(rows, kThreads);
+    k_spmv_sell<T, CC, SKIP, ACC, ORD, 4><<<grid, kThreads, 0, st>>>(
+        m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0,
+        p1, m->n_rows);
+    return 0;
+}
+
+template <typename T, int CC, bool SKIP>
+int dispatch_acc(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1, int acc,
+                 int ord, cudaStream_t st) {
+    if (acc) {
+        return ord ? dispatch_u<T, CC, SKIP, true, 1>(m, x, y, p0, p1, st)
+                   : dispatch_u<T, CC, SKIP, true, 0>(m, x, y, p0, p1, st);
+    }
+    return ord ? dispatch_u<T, CC, SKIP, false, 1>(m, x, y, p0, p1, st)
+               : dispatch_u<T, CC, SKIP, false, 0>(m, x, y, p0, p1, st);
+}
+
+template <typename T>
+int dispatch_sell(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1, int acc,
+                  int ord, cudaStream_t st) {
+    const bool skip = m->variant == SELLB_VARIANT_PAD_SKIP && m->rl;
+    if (m->C == 32) {
+        return skip ? dispatch_acc<T, 32, true>(m, x, y, p0, p1, acc, ord, st)
+                    : dispatch_acc<T, 32, false>(m, x, y, p0, p1, acc, ord, st);
+    }
+    return skip ? dispatch_acc<T, 0, true>(m, x, y, p0, p1, acc, ord, st)
+                : dispatch_acc<T, 0, false>(m, x, y, p0, p1, acc, ord, st);
+}
+
+}  // namespace
+
+namespace sellb {
+
+int launch_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
+                int accumulate, int out_order, cudaStream_t st) {
+    if (c0 < 0 || c1 > m->n_chunks || c0 > c1)
+        return set_error(SELLB_EPARAM, "chunk range [%lld, %lld) outside [0, %lld)",
+                         (long long)c0, (long long)c1, (long long)m->n_chunks);
+    if (out_order == SELLB_ORDER_ORIGINAL && !m->order)
+        return set_error(SELLB_EPARAM, "original-order output needs the row permutation");
+    if (c0 == c1) return 0;
+    int rc = m->dtype == SELLB_F32
+                 ? dispatch_sell<float>(m, x, y, c0 * m->C, c1 * m->C, accumulate, out_order, st)
+                 : dispatch_sell<double>(m, x, y, c0 * m->C, c1 * m->C, accumulate, out_order, st);
+    if (rc) return rc;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_error(SELLB_ERESOURCE, "spmv launch failed: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+int launch_spmv_list(const sellb_mat* m, const int32_t* ids, int64_t n_ids, const void* x,
+                     void* y, int accumulate, cudaStream_t st) {
+    if (n_ids <= 0) return 0;
+    const bool skip = m->variant == SELLB_VARIANT_PAD_SKIP && m->rl;
+    const unsigned grid = (unsigned)grid_for(n_ids * m->C, kThreads);
+#define SELLB_LIST(T, S, A)                                                                   \
+    k_spmv_sell_list<T, S, A><<<grid, kThreads, 0, st>>>(m->cs, m->cl, m->rl, m->col,         \
+                                                         (const T*)m->val, (const T*)x,      \
+                                                         (T*)y, ids, n_ids, m->C)
+    if (m->dtype == SELLB_F32) {
+        if (skip) { if (accumulate) SELLB_LIST(float, true, true); else SELLB_LIST(float, true, false); }
+        else { if (accumulate) SELLB_LIST(float, false, true); else SELLB_LIST(float, false, false); }
+    } else {
+        if (skip) { if (accumulate) SELLB_LIST(double, true, true); else SELLB_LIST(double, true, false); }
+        else { if (accumulate) SELLB_LIST(double, false, true); else SELLB_LIST(double, false, false); }
+    }
+#undef SELLB_LIST
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_error(SELLB_ERESOURCE, "spmv launch failed: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+int launch_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val, int32_t dtype,
+                    const void* x, void* y, int64_t r0, int64_t r1, int accumulate, int unrolled,
+                    cudaStream_t st) {
+    if (r1 <= r0) return 0;
+    const unsigned grid = (unsigned)grid_for(r1 - r0, kThreads);
+#define SELLB_CRS(K, T, A) K<T, A><<<grid, kThreads, 0, st>>>(rpt, col, (const T*)val, (const T*)x, (T*)y, r0, r1)
+    if (dtype == SELLB_F32) {
+        if (unrolled) { if (accumulate) SELLB_CRS(k_spmv_crs_unrolled, float, true); else SELLB_CRS(k_spmv_crs_unrolled, float, false); }
+        else { if (accumulate) SELLB_CRS(k_spmv_crs, float, true); else SELLB_CRS(k_spmv_crs, float, false); }
+    } else {
+        if (unrolled) { if (accumulate) SELLB_CRS(k_spmv_crs_unrolled, double, true); else SELLB_CRS(k_spmv_crs_unrolled, double, false); }
+        else { if (accumulate) SELLB_CRS(k_spmv_crs, double, true); else SELLB_CRS(k_spmv_crs, double, false); }
+    }
+#undef SELLB_CRS
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_error(SELLB_ERESOURCE, "crs launch failed: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+}  // namespace sellb
+
+// ===========================================================================
+// ABI
+// ===========================================================================
+extern "C" {
+
+int sellb_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
+               int32_t accumulate, int32_t out_order, void* stream) {
+    clear_error();
+    if (!m || (!x && m->slots) || !y) return set_error(SELLB_EPARAM, "NULL argument");
+    DeviceGuard guard(m->device);
+    return launch_spmv(m, x, y, c0, c1, accumulate, out_order, (cudaStream_t)stream);
+}
+
+int sellb_spmv_chunk_list(const sellb_mat* m, const int32_t* chunk_ids, int64_t n_ids,
+                          const void* x, void* y, int32_t accumulate, void* stream) {
+    clear_error();
+    if (!m || !y || (n_ids && !chunk_ids)) return set_error(SELLB_EPARAM, "NULL argument");
+    DeviceGuard guard(m->device);
+    return launch_spmv_list(m, chunk_ids, n_ids, x, y, accumulate, (cudaStream_t)stream);
+}
+
+int sellb_spmv_host(sellb_mat* m, const void* x_host, void* y_host, int64_t c0, int64_t c1,
+                    int32_t accumulate, int32_t out_order, void* stream) {
+    clear_error();
+    if (!m || !y_host || (!x_host && m->n_cols)) return set_error(SELLB_EPARAM, "NULL argument");
+    if (c0 < 0 || c1 > m->n_chunks || c0 > c1)
+        return set_error(SELLB_EPARAM, "chunk range outside the matrix");
+    DeviceGuard guard(m->device);
+    std::lock_guard<std::mutex> lk(m->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t vs = vsize(m->dtype);
+    const int64_t ny = out_order == SELLB_ORDER_ORIGINAL ? m->n_rows : m->n_pad;
+    if (!m->x_buf) SELLB_CU(cudaMalloc(&m->x_buf, std::max<int64_t>(m->n_cols, 1) * vs));
+    if (!m->y_buf) SELLB_CU(cudaMalloc(&m->y_buf, std::max<int64_t>(m->n_pad, 1) * vs));
+    if (m->n_cols)
+        SELLB_CU(cudaMemcpyAsync(m->x_buf, x_host, m->n_cols * vs, cudaMemcpyHostToDevice, st));
+    // rows touched by the range
+    int64_t y0 = c0 * m->C, y1 = c1 * m->C;
+    if (out_order == SELLB_ORDER_ORIGINAL) { y0 = 0; y1 = ny; }
+    if (accumulate && y1 > y0)
+        SELLB_CU(cudaMemcpyAsync((char*)m->y_buf + y0 * vs, (const char*)y_host + y0 * vs,
+                                 (y1 - y0) * vs, cudaMemcpyHostToDevice, st));
+    if (out_order == SELLB_ORDER_ORIGINAL && !accumulate && (c0 != 0 || c1 != m->n_chunks)) {
+        // rows outside the range keep the caller's values
+        SELLB_CU(cudaMemcpyAsync(m->y_buf, y_host, ny * vs, cudaMemcpyHostToDevice, st));
+    }
+    if (int rc = launch_spmv(m, m->x_buf, m->y_buf, c0, c1, accumulate, out_order, st)) return rc;
+    if (y1 > y0)
+        SELLB_CU(cudaMemcpyAsync((char*)y_host + y0 * vs, (const char*)m->y_buf + y0 * vs,
+                                 (y1 - y0) * vs, cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int sellb_spmv_sell_range_host(const int64_t* cs, const int32_t* cl, int32_t C,
+                               const int32_t* col, const double* val, int64_t n_slots,
+                               int64_t n_chunks, const double* x, int64_t n_x, double* y,
+                               int64_t n_y, int64_t c0, int64_t c1, int32_t accumulate,
+                               int32_t device) {
+    clear_error();
+    if (C < 1) return set_error(SELLB_EPARAM, "chunk height C must be >= 1");
+    if (c0 < 0 || c1 > n_chunks || c0 > c1) return set_error(SELLB_EPARAM, "bad chunk range");
+    if (n_y < n_chunks * (int64_t)C) return set_error(SELLB_EDIM, "y shorter than n_chunks*C");
+    if (c0 == c1) return 0;
+    if (cs[n_chunks] != n_slots) return set_error(SELLB_ESTRUCT, "cs[n_chunks] != len(val)");
+    sellb_mat* m = nullptr;
+    int rc = sellb_import(cs, cl, col, val, nullptr, nullptr, SELLB_F64, n_chunks * C, n_x, C, 1,
+                          n_chunks, 0, device, nullptr, 0, &m);
+    if (rc) return rc;
+    rc = sellb_spmv_host(m, x, y, c0, c1, accumulate, SELLB_ORDER_STORED, nullptr);
+    sellb_free(m);
+    return rc;
+}
+
+int sellb_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val, int32_t dtype,
+                   const void* x, void* y, int64_t r0, int64_t r1, int32_t accumulate,
+                   int32_t unrolled, void* stream) {
+    clear_error();
+    if (!rpt || !y) return set_error(SELLB_EPARAM, "NULL argument");
+    return launch_spmv_crs(rpt, col, val, dtype, x, y, r0, r1, accumulate, unrolled,
+                           (cudaStream_t)stream);
+}
+
+int sellb_spmv_crs_range_host(const int64_t* rpt, int64_t n_rows, const int32_t* col,
+                              const double* val, int64_t nnz, const double* x, int64_t n_x,
+                              double* y, int64_t r0, int64_t r1, int32_t accumulate,
+                              int32_t unrolled, int32_t device) {
+    clear_error();
+    if (r0 < 0 || r1 > n_rows || r0 > r1) return set_error(SELLB_EPARAM, "bad row range");
+    if (r0 == r1) return 0;
+    DeviceGuard guard(device);
+    if (!guard.ok) return set_error(SELLB_ERESOURCE, "cannot select CUDA device %d", device);
+    cudaStream_t st = 0;
+    DBuf d_rpt, d_col, d_val, d_x, d_y;
+    SELLB_CU(d_rpt.alloc((n_rows + 1) * 8, st));
+    SELLB_CU(d_col.alloc(nnz * 4, st));
+    SELLB_CU(d_val.alloc(nnz * 8, st));
+    SELLB_CU(d_x.alloc(n_x * 8, st));
+    SELLB_CU(d_y.alloc(n_rows * 8, st));
+    SELLB_CU(cudaMemcpyAsync(d_rpt.p, rpt, (n_rows + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (nnz) {
+        SELLB_CU(cudaMemcpyAsync(d_col.p, col, nnz * 4, cudaMemcpyHostToDevice, st));
+        SELLB_CU(cudaMemcpyAsync(d_val.p, val, nnz * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (n_x) SELLB_CU(cudaMemcpyAsync(d_x.p, x, n_x * 8, cudaMemcpyHostToDevice, st));
+    if (accumulate)
+        SELLB_CU(cudaMemcpyAsync(d_y.as<double>() + r0, y + r0, (r1 - r0) * 8,
+                                 cudaMemcpyHostToDevice, st));
+    if (int rc = launch_spmv_crs(d_rpt.as<int64_t>(), d_col.as<int32_t>(), d_val.p, SELLB_F64,
+                                 d_x.p, d_y.p, r0, r1, accumulate, unrolled, st))
+        return rc;
+    SELLB_CU(cudaMemcpyAsync(y + r0, d_y.as<double>() + r0, (r1 - r0) * 8,
+                             cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+// sellb_util.cu -- error state, device queries, bandwidth microbenchmark
+// kernels (analogs of membench.py:52-116 / _kernels.pyx:142-170) and pinned
+// host buffers for the end-to-end path.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "sellb_internal.cuh"
+
+namespace sellb {
+
+static thread_local char g_err[512] = {0};
+
+int set_error(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+void clear_error() { g_err[0] = 0; }
+
+}  // namespace sellb
+
+using namespace sellb;
+
+namespace {
+
+// read-reduce: each thread keeps 4 independent partial sums over 16-byte
+// vector loads (grid-stride), block reduce in shared memory, one partial per
+// block; a second single-block pass combines the partials (deterministic).
+__global__ void __launch_bounds__(256) k_read_sum(const double* __restrict__ a, int64_t n,
+                                                  double* __restrict__ partial) {
+    __shared__ double sh[256];
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    const int64_t n2 = n / 2;
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; i + stride < n2; i += 2 * stride) {
+        double2 u = __ldcs(a2 + i);
+        double2 v = __ldcs(a2 + i + stride);
+        s0 += u.x; s1 += u.y; s2 += v.x; s3 += v.y;
+    }
+    if (i < n2) { double2 u = __ldcs(a2 + i); s0 += u.x; s1 += u.y; }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s0 += a[n - 1];
+    sh[threadIdx.x] = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_sum_partials(const double* __restrict__ partial, int n, double* out) {
+    __shared__ double sh[1024];
+    double s = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+__global__ void __launch_bounds__(256) k_copy(const double* __restrict__ src,
+                                              double* __restrict__ dst, int64_t n) {
+    const int64_t n2 = n / 2;
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; i < n2; i += stride) __stcs(d2 + i, __ldcs(s2 + i));
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) dst[n - 1] = src[n - 1];
+}
+
+__global__ void k_touch(uint4* __restrict__ p, int64_t n, unsigned v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; i < n; i += stride) p[i] = make_uint4(v, v + 1, v + 2, v + 3);
+}
+
+int grid_fill() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms * 8;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sellb_last_error(void) { return sellb::g_err; }
+
+int sellb_version(void) { return 10000; }
+
+int sellb_device_count(int32_t* n) {
+    clear_error();
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        if (n) *n = 0;
+        return set_error(SELLB_ERESOURCE, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    if (n) *n = c;
+    return 0;
+}
+
+int sellb_read_sum(const double* a, int64_t n, double* out_host, void* stream) {
+    clear_error();
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = grid_fill();
+    DBuf part, res;
+    SELLB_CU(part.alloc(blocks * sizeof(double), st));
+    SELLB_CU(res.alloc(sizeof(double), st));
+    k_read_sum<<<blocks, 256, 0, st>>>(a, n, part.as<double>());
+    k_sum_partials<<<1, 1024, 0, st>>>(part.as<double>(), blocks, res.as<double>());
+    SELLB_CU(cudaGetLastError());
+    if (out_host) {
+        SELLB_CU(cudaMemcpyAsync(out_host, res.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+    }
+    return 0;
+}
+
+int sellb_copy(const double* src, double* dst, int64_t n, void* stream) {
+    clear_error();
+    cudaStream_t st = (cudaStream_t)stream;
+    k_copy<<<grid_fill(), 256, 0, st>>>(src, dst, n);
+    SELLB_CU(cudaGetLastError());
+    return 0;
+}
+
+int sellb_l2_flush(void* scratch, int64_t bytes, void* stream) {
+    clear_error();
+    static unsigned counter = 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_touch<<<grid_fill(), 256, 0, st>>>((uint4*)scratch, bytes / 16, counter++);
+    SELLB_CU(cudaGetLastError());
+    return 0;
+}
+
+int sellb_host_alloc(size_t bytes, void** out) {
+    clear_error();
+    if (!out) return set_error(SELLB_EPARAM, "NULL out");
+    SELLB_CU(cudaMallocHost(out, bytes ? bytes : 16));
+    return 0;
+}
+
+int sellb_host_free(void* p) {
+    clear_error();
+    if (p) SELLB_CU(cudaFreeHost(p));
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,183 @@
+"""Generate the golden parity fixtures from the REFERENCE itself.
+
+Run in the build container (needs /root/reference, which does not exist on
+the GPU box):
+
+    make -C oracle ref            # builds oracle/_ref/_kernels*.so
+    python tests/golden/make_golden.py
+
+It imports the reference package from /root/reference/pkg/src (its NumPy
+`crs_to_sell`, `coo_to_crs`, generators and test fixtures' random-matrix
+recipe) and the reference's own compiled kernel core from oracle/_ref, and
+writes one small .npz per case into tests/golden/.  The fixtures are
+committed; tests/test_oracle_golden.py pins the C oracle to them and the GPU
+tests pin the CUDA path to them.
+"""
+
+import os
+import sys
+import importlib.util
+import glob
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+os.environ["SELLKIT_BACKEND"] = "python"
+
+import sellkit  # noqa: E402  (the reference)
+from sellkit import (COOMatrix, canonicalize_coo, coo_to_crs, crs_to_sell,  # noqa: E402
+                     gen_skewed, gen_worst_case, gen_banded, get_kernels,
+                     ParameterError)
+
+
+def load_ref_compiled():
+    hits = glob.glob(os.path.join(REPO, "oracle", "_ref", "_kernels*.so"))
+    if not hits:
+        raise SystemExit("build oracle/_ref first: make -C oracle ref")
+    spec = importlib.util.spec_from_file_location("_kernels", hits[0])
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def random_coo(rng, n_rows, n_cols, nnz_target, allow_zero_values=False):
+    """Reference recipe: pkg/tests/conftest.py:10-23."""
+    nnz_target = min(nnz_target, n_rows * n_cols)
+    if nnz_target <= 0 or n_rows == 0 or n_cols == 0:
+        return COOMatrix(n_rows, n_cols, np.empty(0, np.int32),
+                         np.empty(0, np.int32), np.empty(0, np.float64))
+    flat = rng.choice(n_rows * n_cols, size=nnz_target, replace=False)
+    rows = (flat // n_cols).astype(np.int32)
+    cols = (flat % n_cols).astype(np.int32)
+    vals = rng.uniform(-1.0, 1.0, size=nnz_target)
+    if allow_zero_values:
+        vals[rng.random(nnz_target) < 0.05] = 0.0
+    return canonicalize_coo(COOMatrix(n_rows, n_cols, rows, cols, vals))
+
+
+def powerlaw_crs(rng, n, mean_base=4, lmax=150):
+    lengths = np.clip(np.floor(mean_base * (1 + rng.pareto(2.0, n))), 1,
+                      min(lmax, n)).astype(np.int64)
+    rows = np.repeat(np.arange(n), lengths)
+    starts = rng.integers(0, n, size=n)
+    starts = np.minimum(starts, n - lengths)
+    k = np.arange(lengths.sum()) - np.repeat(np.cumsum(lengths) - lengths, lengths)
+    cols = np.repeat(starts, lengths) + k
+    vals = rng.uniform(-1, 1, len(rows))
+    return coo_to_crs(COOMatrix(n, n, rows, cols, vals))
+
+
+def example_crs():
+    """pkg/tests/test_formats.py:13-24."""
+    rows = np.array([0, 0, 0, 1, 2, 2, 3], np.int32)
+    cols = np.array([0, 1, 2, 1, 0, 3, 2], np.int32)
+    vals = np.array([1.0, 2, 3, 4, 5, 6, 7])
+    return coo_to_crs(COOMatrix(4, 4, rows, cols, vals))
+
+
+def cases():
+    rng = np.random.default_rng(20240901)
+    yield "example_C2_s1", example_crs(), 2, 1, 1, False
+    yield "example_C2_s4", example_crs(), 2, 4, 1, False
+    m = coo_to_crs(random_coo(rng, 60, 60, 360))
+    for C in (1, 2, 4, 8, 16, 32):
+        for sigma in sorted({1, C, 4 * C, 60}):
+            if C < sigma < 60 and sigma % C:
+                continue
+            yield f"rand60_C{C}_s{sigma}", m, C, sigma, 1, False
+    yield "rand60_C32_sbig", m, 32, 10 ** 9, 1, False
+    yield "rect30x70_C8_s16", coo_to_crs(random_coo(rng, 30, 70, 250)), 8, 16, 1, False
+    yield "rect70x30_C4_s16", coo_to_crs(random_coo(rng, 70, 30, 400)), 4, 16, 1, False
+    mp = coo_to_crs(random_coo(rng, 60, 60, 360))
+    yield "permcols_C4_sN", mp, 4, 60, 1, True
+    yield "permcols_C8_s16", mp, 8, 16, 1, True
+    ma = coo_to_crs(random_coo(rng, 45, 45, 400))
+    yield "align64_C2_s1", ma, 2, 1, 64, False
+    yield "align64_C4_s8", ma, 4, 8, 64, False
+    yield "align64_C3_s1", ma, 3, 1, 64, False
+    yield "align64_C32_sN", ma, 32, 45, 64, False
+    yield "zeros_C8_s32", coo_to_crs(random_coo(rng, 90, 90, 900, allow_zero_values=True)), 8, 32, 1, False
+    rows = np.array([0, 0, 4], np.int32)
+    cols = np.array([1, 3, 2], np.int32)
+    yield "emptyrows_C2_s5", coo_to_crs(COOMatrix(5, 5, rows, cols, np.array([1.0, 2, 3]))), 2, 5, 1, False
+    yield "empty_C2_s1", coo_to_crs(COOMatrix(3, 3, np.empty(0, np.int32), np.empty(0, np.int32), np.empty(0))), 2, 1, 1, False
+    yield "zero_rows_C4_s1", coo_to_crs(COOMatrix(0, 5, np.empty(0, np.int32), np.empty(0, np.int32), np.empty(0))), 4, 1, 1, False
+    yield "small_n3_C32_s1", coo_to_crs(random_coo(rng, 3, 3, 6)), 32, 1, 1, False
+    yield "small_n3_C32_sN", coo_to_crs(random_coo(rng, 3, 3, 6)), 32, 64, 1, False
+    yield "ties_C2_s4", coo_to_crs(COOMatrix(4, 1, np.arange(4), np.zeros(4, int), np.ones(4))), 2, 4, 1, False
+    wc = coo_to_crs(gen_worst_case(8, 4))
+    yield "worst8x4_C4_s1", wc, 4, 1, 1, False
+    yield "worst8x4_C4_s16", wc, 4, 16, 1, False
+    sk = coo_to_crs(gen_skewed(700, base_len=3, spike_len=200, spike_count=4))
+    for sigma in (1, 32, 128, 700):
+        yield f"skewed700_C32_s{sigma}", sk, 32, sigma, 1, False
+    pl = powerlaw_crs(rng, 1200)
+    for C, sigma in ((32, 1), (32, 128), (32, 512), (32, 1200), (8, 64),
+                     (16, 256), (64, 256), (128, 512)):
+        yield f"powerlaw1200_C{C}_s{sigma}", pl, C, sigma, 1, False
+    bd = coo_to_crs(gen_banded(300, 4, fill=0.6))
+    yield "banded300_C32_s1", bd, 32, 1, 1, False
+    yield "banded300_C32_s64", bd, 32, 64, 1, False
+
+
+def main():
+    comp = load_ref_compiled()
+    py = get_kernels("python")
+    out_dir = HERE
+    for f in glob.glob(os.path.join(out_dir, "case_*.npz")):
+        os.remove(f)
+    idx = 0
+    xrng = np.random.default_rng(12345)
+    for name, m, C, sigma, align, permute in cases():
+        s = crs_to_sell(m, C, sigma, align_bytes=align, permute_cols=permute)
+        x = xrng.uniform(-1, 1, m.n_cols)
+        y = np.zeros(s.n_rows_padded)
+        comp.spmv_sell_range(s.cs, s.cl, s.C, s.col, s.val, x, y, 0, s.n_chunks, False)
+        y_py = np.zeros(s.n_rows_padded)
+        py.spmv_sell_range(s.cs, s.cl, s.C, s.col, s.val, x, y_py, 0, s.n_chunks, False)
+        assert np.array_equal(y, y_py), name
+        y0 = xrng.uniform(-1, 1, s.n_rows_padded)
+        y_acc = y0.copy()
+        comp.spmv_sell_range(s.cs, s.cl, s.C, s.col, s.val, x, y_acc, 0, s.n_chunks, True)
+        # x[0] non-finite: padded slots read x[0] (formats.py:362-363)
+        x_inf = x.copy()
+        if len(x_inf):
+            x_inf[0] = np.inf
+        y_inf = np.zeros(s.n_rows_padded)
+        with np.errstate(invalid="ignore"):
+            comp.spmv_sell_range(s.cs, s.cl, s.C, s.col, s.val, x_inf, y_inf, 0, s.n_chunks, False)
+        y_crs = np.zeros(m.n_rows)
+        comp.spmv_crs_range(m.rpt, m.col, m.val, x, y_crs, 0, m.n_rows, False)
+        y_crs_u = np.zeros(m.n_rows)
+        comp.spmv_crs_unrolled_range(m.rpt, m.col, m.val, x, y_crs_u, 0, m.n_rows, False)
+        np.savez_compressed(
+            os.path.join(out_dir, f"case_{idx:03d}_{name}.npz"),
+            name=name, n_rows=m.n_rows, n_cols=m.n_cols, C=C, sigma=sigma,
+            align_bytes=align, permute_cols=permute,
+            rpt=m.rpt, col_in=m.col, val_in=m.val,
+            n_rows_padded=s.n_rows_padded, n_chunks=s.n_chunks,
+            cs=s.cs, cl=s.cl, col=s.col, val=s.val, perm=s.perm,
+            row_lengths=s.row_lengths, beta=sellkit.chunk_occupancy(s),
+            x=x, y=y, y0=y0, y_acc=y_acc, x_inf=x_inf, y_inf=y_inf,
+            y_crs=y_crs, y_crs_unrolled=y_crs_u)
+        idx += 1
+    # parameter-error cases (formats.py:309-332): (n_rows, C, sigma, align)
+    m = coo_to_crs(random_coo(np.random.default_rng(5), 100, 100, 500))
+    errs = []
+    for C, sigma, align, permute in ((4, 6, 1, False), (0, 1, 1, False),
+                                     (-2, 1, 1, False), (4, 0, 1, False),
+                                     (4, 8, 32, False), (32, 48, 1, False)):
+        try:
+            crs_to_sell(m, C, sigma, align_bytes=align, permute_cols=permute)
+            errs.append((C, sigma, align, 0))
+        except ParameterError:
+            errs.append((C, sigma, align, 1))
+    np.savez_compressed(os.path.join(out_dir, "param_errors.npz"),
+                        n_rows=100, cases=np.array(errs, np.int64))
+    print(f"wrote {idx} cases to {out_dir}")
+
+
+if __name__ == "__main__":
+    main()
