@@ -320,6 +320,12 @@ def run_ours(args):
         launch()
     torch.cuda.synchronize()
 
+    # inputs smaller than ~2x L2 are flushed between steps (timing hygiene)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = None
+    if v_alg < 2 * l2_bytes:
+        flush = torch.empty(4 * l2_bytes, dtype=torch.uint8, device=dev)
+
     # timed region: K steps, per-step events on the launching stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -331,6 +337,8 @@ def run_ours(args):
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     for i in range(args.steps):
+        if flush is not None:           # outside the kernel's event pair
+            _lib.check(lib.sellb_l2_flush(flush.data_ptr(), flush.numel(), sp))
         ev[i][0].record(stream)
         launch()
         ev[i][1].record(stream)
@@ -340,7 +348,9 @@ def run_ours(args):
     total_ms = t_start.elapsed_time(t_end)
     per = [a.elapsed_time(b) for a, b in ev]
     kern_ms = statistics.mean(per)
-    value = 2.0 * nnz * args.steps / (total_ms / 1e3) / 1e9
+    # with an L2 flush between steps the step time is the SpMV's own events
+    step_ms = kern_ms if flush is not None else total_ms / args.steps
+    value = 2.0 * nnz / (step_ms / 1e3) / 1e9
     peak, peak_kind = measured_peaks()
     achieved = v_alg / (kern_ms / 1e3) / 1e9
 
@@ -378,13 +388,15 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
+        "ms_per_step": round(step_ms, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": f"{desc}, SELL-32-{sigma}", "C": 32, "sigma": sigma,
                    "n_rows": crs.n_rows, "nnz": nnz, "slots": slots,
                    "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
-                   "l2": "inputs larger than L2 (V_alg %.0f MB > 126 MB)" % (v_alg / 1e6)
-                   if v_alg > 126e6 else "L2-resident (V_alg < L2); no flush",
+                   "l2": ("flushed between steps (%d MB scratch write); value from the "
+                          "SpMV's own events" % (4 * l2_bytes // 2**20)) if flush is not None
+                   else "inputs larger than L2 (V_alg %.0f MB > %d MB L2)" % (
+                       v_alg / 1e6, l2_bytes // 2**20),
                    "build_s": round(build_s, 4), "parity_vs_oracle": parity},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -397,7 +409,7 @@ def run_ours(args):
                 "matches_device": e2e_ok},
         "cpu_baseline": cpu,
         "clocks": clk,
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * (2 if flush is not None else 1),
     }
     print(json.dumps(line), flush=True)
     return 0
