@@ -172,6 +172,19 @@ int sellb_copy(const double* src_dev, double* dst_dev, int64_t n, void* stream);
 /* Overwrite a scratch buffer larger than L2 (timing hygiene). */
 int sellb_l2_flush(void* scratch_dev, int64_t bytes, void* stream);
 
+/* Padding fix-up of the row-partitioned path: the reference adds 0*x[0]
+ * for every padded slot, which only matters when x[0] is not finite.  With
+ * *x0 (device) not finite, every stored row with padding becomes
+ * y[p] + 0*x0 (NaN); with finite *x0 the kernel writes nothing. */
+int sellb_pad_fixup(const sellb_mat* m, const void* x0, void* y, void* stream);
+
+/* Halo pack / unpack for the row-partitioned multi-GPU SpMV (dist.py):
+ * out[k] = x[idx[k]]  and  x[idx[k]] = in[k]  (k < n), on `stream`. */
+int sellb_gather(const void* x, const int32_t* idx, void* out, int64_t n, int32_t dtype,
+                 void* stream);
+int sellb_scatter(const void* in, const int32_t* idx, void* x, int64_t n, int32_t dtype,
+                  void* stream);
+
 /* Pinned host buffers for the end-to-end path. */
 int sellb_host_alloc(size_t bytes, void** out);
 int sellb_host_free(void* p);

@@ -31,7 +31,8 @@ EXPORTED = (
     "sellb_spmv_chunk_list", "sellb_spmv_host", "sellb_spmv_sell_range_host",
     "sellb_spmv_crs_range_host", "sellb_spmv_crs", "sellb_chunk_occupancy",
     "sellb_sector_occupancy", "sellb_read_sum", "sellb_copy", "sellb_l2_flush",
-    "sellb_host_alloc", "sellb_host_free",
+    "sellb_host_alloc", "sellb_host_free", "sellb_gather", "sellb_scatter",
+    "sellb_pad_fixup",
 )
 
 
@@ -87,6 +88,9 @@ _PROTOS = {
     "sellb_copy": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
     "sellb_l2_flush": (ctypes.c_int, [_vp, _i64, _vp]),
     "sellb_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(_vp)]),
+    "sellb_gather": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "sellb_scatter": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "sellb_pad_fixup": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "sellb_host_free": (ctypes.c_int, [_vp]),
 }
 

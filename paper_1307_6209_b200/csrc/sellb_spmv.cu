@@ -180,6 +180,18 @@ k_spmv_sell_list(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     y[p] = ACC ? Arith<T>::add(y[p], sum) : sum;
 }
 
+// Padding fix-up for the row-partitioned path (see sellb_pad_fixup).
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+k_pad_fixup(const int32_t* __restrict__ cl, const int32_t* __restrict__ rl, int64_t C,
+            int64_t n_pad, const T* __restrict__ x0, T* __restrict__ y) {
+    const T v = *x0;
+    if (isfinite(v)) return;
+    const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (p >= n_pad) return;
+    if (rl[p] < cl[p / C]) y[p] = Arith<T>::add(y[p], Arith<T>::mul(T(0), v));
+}
+
 // CRS kernels (_kernels.pyx:17-62), one thread per row, reference order.
 template <typename T, bool ACC>
 __global__ void __launch_bounds__(kThreads)
@@ -339,6 +351,26 @@ int sellb_spmv_chunk_list(const sellb_mat* m, const int32_t* chunk_ids, int64_t 
     if (!m || !y || (n_ids && !chunk_ids)) return set_error(SELLB_EPARAM, "NULL argument");
     DeviceGuard guard(m->device);
     return launch_spmv_list(m, chunk_ids, n_ids, x, y, accumulate, (cudaStream_t)stream);
+}
+
+int sellb_pad_fixup(const sellb_mat* m, const void* x0, void* y, void* stream) {
+    clear_error();
+    if (!m || !x0 || !y) return set_error(SELLB_EPARAM, "NULL argument");
+    if (!m->rl) return set_error(SELLB_EPARAM, "pad fix-up needs row_lengths");
+    if (m->n_pad == 0) return 0;
+    DeviceGuard guard(m->device);
+    const unsigned grid = (unsigned)grid_for(m->n_pad, kThreads);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (m->dtype == SELLB_F32)
+        k_pad_fixup<float><<<grid, kThreads, 0, st>>>(m->cl, m->rl, m->C, m->n_pad,
+                                                     (const float*)x0, (float*)y);
+    else
+        k_pad_fixup<double><<<grid, kThreads, 0, st>>>(m->cl, m->rl, m->C, m->n_pad,
+                                                      (const double*)x0, (double*)y);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_error(SELLB_ERESOURCE, "fix-up launch failed: %s", cudaGetErrorString(e));
+    return 0;
 }
 
 int sellb_spmv_host(sellb_mat* m, const void* x_host, void* y_host, int64_t c0, int64_t c1,

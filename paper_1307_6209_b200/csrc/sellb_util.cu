@@ -83,6 +83,20 @@ __global__ void k_touch(uint4* __restrict__ p, int64_t n, unsigned v) {
     for (; i < n; i += stride) p[i] = make_uint4(v, v + 1, v + 2, v + 3);
 }
 
+template <typename T>
+__global__ void k_gather(const T* __restrict__ x, const int32_t* __restrict__ idx,
+                         T* __restrict__ out, int64_t n) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[k] = x[idx[k]];
+}
+
+template <typename T>
+__global__ void k_scatter(const T* __restrict__ in, const int32_t* __restrict__ idx,
+                          T* __restrict__ x, int64_t n) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) x[idx[k]] = in[k];
+}
+
 int grid_fill() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -140,6 +154,34 @@ int sellb_l2_flush(void* scratch, int64_t bytes, void* stream) {
     static unsigned counter = 1;
     cudaStream_t st = (cudaStream_t)stream;
     k_touch<<<grid_fill(), 256, 0, st>>>((uint4*)scratch, bytes / 16, counter++);
+    SELLB_CU(cudaGetLastError());
+    return 0;
+}
+
+int sellb_gather(const void* x, const int32_t* idx, void* out, int64_t n, int32_t dtype,
+                 void* stream) {
+    clear_error();
+    if (n <= 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned g = (unsigned)grid_for(n, 256);
+    if (dtype == SELLB_F32)
+        k_gather<float><<<g, 256, 0, st>>>((const float*)x, idx, (float*)out, n);
+    else
+        k_gather<double><<<g, 256, 0, st>>>((const double*)x, idx, (double*)out, n);
+    SELLB_CU(cudaGetLastError());
+    return 0;
+}
+
+int sellb_scatter(const void* in, const int32_t* idx, void* x, int64_t n, int32_t dtype,
+                  void* stream) {
+    clear_error();
+    if (n <= 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned g = (unsigned)grid_for(n, 256);
+    if (dtype == SELLB_F32)
+        k_scatter<float><<<g, 256, 0, st>>>((const float*)in, idx, (float*)x, n);
+    else
+        k_scatter<double><<<g, 256, 0, st>>>((const double*)in, idx, (double*)x, n);
     SELLB_CU(cudaGetLastError());
     return 0;
 }

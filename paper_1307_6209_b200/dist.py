@@ -1,0 +1,463 @@
+"""Row-partitioned multi-GPU SELL-C-sigma SpMV with a halo exchange of x
+(SURVEY.md §8(e)); the reference has no distributed mode.
+
+Layout: rank k owns the contiguous rows [b_k, b_{k+1}) (boundaries are
+multiples of lcm(C, sigma_eff), balanced by nnz) and the matching slice of
+x.  Each rank builds its block's SELL-C-sigma on its own GPU with *global*
+column indices -- by the block-decomposition property the
+arrays equal the corresponding slice of the single-GPU build -- and keeps a
+full-length replica ``x_full`` whose owned part is written locally and whose
+halo entries arrive from the owners.
+
+One SpMV (``DistSpmv.step``):
+  1. post the halo exchange (NCCL send/recv of the needed x entries, one
+     grouped batch; contiguous halos go straight from/into x_full slices,
+     scattered ones through gather/scatter kernels),
+  2. run the *interior* chunks (every column owned) while it is in flight,
+  3. wait, unpack, run the *boundary* chunks,
+  4. apply the padding fix-up with rank 0's x[0] (the reference adds
+     0*x[0] per padded slot; only a non-finite x[0] changes y).
+Every row is summed by one thread in slot order, so y is bitwise identical
+to the single-GPU product and to the reference.
+
+The communication and partition logic is backend-agnostic: on GPUs it runs
+over NCCL with the CUDA kernels (``CudaEngine``); the CPU tests drive the
+same code over gloo with a checker engine built on the oracle.
+"""
+
+import math
+
+import numpy as np
+
+from .errors import ParameterError
+
+try:
+    import torch
+    import torch.distributed as tdist
+except ImportError:  # pragma: no cover
+    torch = None
+    tdist = None
+
+
+# ---------------------------------------------------------------------------
+# partition
+# ---------------------------------------------------------------------------
+
+def sigma_effective(n_rows, C, sigma):
+    """formats.py:325-334 (None when sigma >= n: one global scope)."""
+    if sigma <= C:
+        return 1
+    if sigma >= n_rows:
+        return None
+    if sigma % C:
+        raise ParameterError(
+            f"sigma ({sigma}) must be a multiple of C ({C}) when C < sigma < n_rows")
+    return sigma
+
+
+def partition_rows(rpt, world, C=32, sigma=1):
+    """Contiguous row blocks for ``world`` ranks, boundaries at multiples of
+    lcm(C, sigma_eff), balanced by nonzeros.  Returns int64 bounds[world+1].
+
+    A global scope (sigma >= n_rows) does not decompose; it is rejected for
+    world > 1 (sort per block with sigma <= rows per rank instead)."""
+    rpt = np.asarray(rpt, dtype=np.int64)
+    n = len(rpt) - 1
+    s_eff = sigma_effective(n, C, sigma)
+    if s_eff is None:
+        if world > 1:
+            raise ParameterError("sigma >= n_rows (global sort) cannot be row-partitioned")
+        s_eff = 1
+    unit = C * s_eff // math.gcd(C, s_eff)
+    nnz = int(rpt[-1])
+    bounds = [0]
+    for k in range(1, world):
+        target = nnz * k / world
+        r = int(np.searchsorted(rpt, target, side="left"))
+        r = int(round(r / unit)) * unit
+        r = min(max(r, bounds[-1]), n)
+        bounds.append(r)
+    bounds.append(n)
+    return np.array(bounds, dtype=np.int64)
+
+
+# ---------------------------------------------------------------------------
+# halo plan
+# ---------------------------------------------------------------------------
+
+def _contiguous(idx):
+    return len(idx) > 0 and int(idx[-1]) - int(idx[0]) + 1 == len(idx)
+
+
+class HaloPlan:
+    """Who sends which x entries to whom.
+
+    ``recv[p]``: sorted global indices this rank needs from rank p;
+    ``send[p]``: sorted global indices (owned here) rank p needs from us.
+    Built with one all_gather of the request lists (setup only)."""
+
+    def __init__(self, rank, world, bounds, recv, send, need_x0):
+        self.rank, self.world = rank, world
+        self.bounds = np.asarray(bounds, dtype=np.int64)
+        self.recv = recv
+        self.send = send
+        self.need_x0 = need_x0          # rank -> bool: that rank needs x[0]
+
+    @staticmethod
+    def requests(col_local, bounds, rank):
+        """The x entries this rank's block reads but does not own, by owner."""
+        bounds = np.asarray(bounds, dtype=np.int64)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        col = np.asarray(col_local)
+        remote = np.unique(col[(col < r0) | (col >= r1)]).astype(np.int64)
+        owner = np.searchsorted(bounds, remote, side="right") - 1
+        return {int(p): remote[owner == p].astype(np.int32)
+                for p in np.unique(owner) if p != rank}
+
+    @classmethod
+    def from_requests(cls, rank, world, bounds, gathered):
+        """gathered[p] = (requests of rank p, rank p has padding)."""
+        recv = gathered[rank][0]
+        send = {}
+        for p in range(world):
+            if p == rank:
+                continue
+            want = gathered[p][0].get(rank)
+            if want is not None and len(want):
+                send[p] = np.asarray(want, dtype=np.int32)
+        need_x0 = {p: bool(gathered[p][1]) and p != 0 for p in range(world)}
+        return cls(rank, world, bounds, recv, send, need_x0)
+
+    @classmethod
+    def build(cls, col_local, bounds, rank, world, has_padding, group=None):
+        recv = cls.requests(col_local, bounds, rank)
+        gathered = [None] * world
+        tdist.all_gather_object(gathered, (recv, bool(has_padding)), group=group)
+        return cls.from_requests(rank, world, bounds, gathered)
+
+    def halo_entries(self):
+        return int(sum(len(v) for v in self.recv.values()))
+
+    def bytes_per_step(self, value_bytes=8):
+        """Bytes this rank receives per SpMV (x halo + x[0])."""
+        return value_bytes * (self.halo_entries() + (1 if self.need_x0.get(self.rank) else 0))
+
+
+def classify_chunks(rpt_local, col_local, perm, C, r0, r1):
+    """Boundary flag per chunk: a stored row with a non-owned column makes
+    its chunk wait for the halo.  Returns (interior_ranges, boundary_ranges)
+    as lists of [c0, c1) runs."""
+    rpt_local = np.asarray(rpt_local, dtype=np.int64)
+    n = len(rpt_local) - 1
+    col = np.asarray(col_local)
+    remote = ((col < r0) | (col >= r1)).astype(np.int64)
+    cnt = np.zeros(len(remote) + 1, dtype=np.int64)
+    np.cumsum(remote, out=cnt[1:])
+    per_row = (cnt[rpt_local[1:]] - cnt[rpt_local[:-1]]) > 0
+    n_chunks = (n + C - 1) // C
+    bnd = np.zeros(n_chunks, dtype=bool)
+    if n:
+        np.logical_or.at(bnd, np.asarray(perm, dtype=np.int64)[per_row] // C, True)
+    return _runs(~bnd), _runs(bnd)
+
+
+def _runs(mask):
+    runs = []
+    i, n = 0, len(mask)
+    while i < n:
+        if mask[i]:
+            j = i
+            while j < n and mask[j]:
+                j += 1
+            runs.append((i, j))
+            i = j
+        else:
+            i += 1
+    return runs
+
+
+# ---------------------------------------------------------------------------
+# engines: the local multiply
+# ---------------------------------------------------------------------------
+
+class CudaEngine:
+    """Local SELL multiply on this rank's GPU through libsellb200.so."""
+
+    def __init__(self, sell, device):
+        from . import _lib
+        self.lib = _lib.load()
+        self.check = _lib.check
+        self.sell = sell
+        self.handle = sell.handle
+        self.device = device
+        self.dtype_code = _lib.SELLB_F32 if sell.dtype == np.float32 else _lib.SELLB_F64
+        self.launches = 0
+
+    def stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def run_ranges(self, ranges, x_full, y):
+        st = self.stream()
+        for c0, c1 in ranges:
+            self.check(self.lib.sellb_spmv(self.handle, x_full.data_ptr(), y.data_ptr(),
+                                           c0, c1, 0, 0, st))
+            self.launches += 1
+
+    def gather(self, x_full, idx_dev, out):
+        self.check(self.lib.sellb_gather(x_full.data_ptr(), idx_dev.data_ptr(),
+                                         out.data_ptr(), idx_dev.numel(), self.dtype_code,
+                                         self.stream()))
+        self.launches += 1
+
+    def scatter(self, buf, idx_dev, x_full):
+        self.check(self.lib.sellb_scatter(buf.data_ptr(), idx_dev.data_ptr(),
+                                          x_full.data_ptr(), idx_dev.numel(), self.dtype_code,
+                                          self.stream()))
+        self.launches += 1
+
+    def pad_fixup(self, x0_buf, y):
+        self.check(self.lib.sellb_pad_fixup(self.handle, x0_buf.data_ptr(), y.data_ptr(),
+                                            self.stream()))
+        self.launches += 1
+
+
+# ---------------------------------------------------------------------------
+# the distributed SpMV
+# ---------------------------------------------------------------------------
+
+class DistSpmv:
+    """One rank's share of y = A x.
+
+    ``engine`` runs local chunk ranges (CudaEngine on GPUs); ``sell_host``
+    supplies n_chunks / row info; x_full / y are torch tensors on the
+    engine's device (CPU tensors under gloo)."""
+
+    def __init__(self, engine, plan, n_chunks, n_pad, n_global, interior, boundary,
+                 has_padding, device, dtype, group=None):
+        self.engine, self.plan = engine, plan
+        self.interior, self.boundary = interior, boundary
+        self.group = group
+        self.device = device
+        r0, r1 = int(plan.bounds[plan.rank]), int(plan.bounds[plan.rank + 1])
+        self.r0, self.r1 = r0, r1
+        self.x_full = torch.zeros(n_global, dtype=dtype, device=device)
+        self.x_local = self.x_full[r0:r1]               # owned slice (a view)
+        self.y = torch.zeros(n_pad, dtype=dtype, device=device)
+        self.has_padding = has_padding
+        self.x0_buf = torch.zeros(1, dtype=dtype, device=device)
+        idx = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)
+        # receive side: contiguous halos land directly in x_full
+        self.recv_ops = []
+        for p, g in sorted(plan.recv.items()):
+            if _contiguous(g):
+                self.recv_ops.append((p, self.x_full[int(g[0]):int(g[-1]) + 1], None))
+            else:
+                self.recv_ops.append((p, torch.empty(len(g), dtype=dtype, device=device),
+                                      idx(g)))
+        self.send_ops = []
+        for p, g in sorted(plan.send.items()):
+            if _contiguous(g):
+                self.send_ops.append((p, self.x_full[int(g[0]):int(g[-1]) + 1], None))
+            else:
+                self.send_ops.append((p, torch.empty(len(g), dtype=dtype, device=device),
+                                      idx(g)))
+        self.x0_peers = [p for p, need in plan.need_x0.items() if need] \
+            if plan.rank == 0 else []
+        self.x0_recv = plan.need_x0.get(plan.rank, False)
+
+    def _post_exchange(self):
+        ops = []
+        for p, buf, gidx in self.send_ops:
+            if gidx is not None:
+                self.engine.gather(self.x_full, gidx, buf)
+            ops.append(tdist.P2POp(tdist.isend, buf, p, group=self.group))
+        for p, buf, _ in self.recv_ops:
+            ops.append(tdist.P2POp(tdist.irecv, buf, p, group=self.group))
+        for p in self.x0_peers:
+            ops.append(tdist.P2POp(tdist.isend, self.x_full[0:1], p, group=self.group))
+        if self.x0_recv:
+            ops.append(tdist.P2POp(tdist.irecv, self.x0_buf, 0, group=self.group))
+        return tdist.batch_isend_irecv(ops) if ops else []
+
+    def step(self):
+        """y_local = A_local x (x_local must hold this rank's x slice)."""
+        works = self._post_exchange()
+        self.engine.run_ranges(self.interior, self.x_full, self.y)
+        for w in works:
+            w.wait()
+        for p, buf, gidx in self.recv_ops:
+            if gidx is not None:
+                self.engine.scatter(buf, gidx, self.x_full)
+        self.engine.run_ranges(self.boundary, self.x_full, self.y)
+        if self.x0_recv and self.has_padding:
+            self.engine.pad_fixup(self.x0_buf, self.y)
+        return self.y
+
+
+def setup(crs_local, bounds, C, sigma, rank, world, device, engine_factory,
+          dtype=None, group=None, plan=None, built=None):
+    """Build this rank's local SELL (through ``engine_factory(crs_local)``,
+    which returns (engine, sell_info)) and the halo plan (collective unless a
+    precomputed ``plan`` is given)."""
+    engine, info = built if built is not None else engine_factory(crs_local)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    perm = info["perm"]
+    has_padding = bool(info["has_padding"])
+    if plan is None:
+        plan = HaloPlan.build(crs_local.col, bounds, rank, world, has_padding, group=group)
+    interior, boundary = classify_chunks(crs_local.rpt, crs_local.col, perm, C, r0, r1)
+    tdt = dtype or torch.float64
+    return DistSpmv(engine, plan, info["n_chunks"], info["n_rows_padded"],
+                    crs_local.n_cols, interior, boundary, has_padding, device, tdt,
+                    group=group)
+
+
+def cuda_engine_factory(C, sigma, device, dtype=None):
+    """engine_factory for GPUs: device build of the local block."""
+    from .formats import crs_to_sell
+
+    def make(crs_local):
+        s = crs_to_sell(crs_local, C, sigma, device=device.index or 0, dtype=dtype)
+        rl = s.row_lengths
+        cl = s.cl
+        has_pad = bool(len(rl) and np.any(rl < np.repeat(cl, C)))
+        info = {"perm": s.perm, "n_chunks": s.n_chunks, "n_rows_padded": s.n_rows_padded,
+                "has_padding": has_pad, "sell": s}
+        return CudaEngine(s, device), info
+    return make
+
+
+# ---------------------------------------------------------------------------
+# benchmark entry (torchrun, one process per GPU)
+# ---------------------------------------------------------------------------
+
+def bench_main(args):
+    """Weak scaling: the 27-point stencil on 128 x 128 x (128 N), one
+    128^3 z-slab per GPU, halo = one 128x128 plane per neighbour."""
+    import json
+    import os
+    import statistics
+    import time
+
+    from . import generate
+    from .model import algorithmic_bytes
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    tdist.init_process_group("nccl", device_id=device)
+    n, nz_per = 128, 128
+    nz = nz_per * world
+    n_glob = n * n * nz
+    C, sigma = 32, args.sigma
+    crs = generate.stencil27_slab(n, nz, rank * nz_per, (rank + 1) * nz_per)
+    bounds = np.arange(world + 1, dtype=np.int64) * (n * n * nz_per)
+    t0 = time.perf_counter()
+    ds = setup(crs, bounds, C, sigma, rank, world, device,
+               cuda_engine_factory(C, sigma, device))
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    x_glob_rng = np.random.default_rng(12345)
+    x_all = x_glob_rng.uniform(-1, 1, n_glob)
+    ds.x_local.copy_(torch.from_numpy(x_all[ds.r0:ds.r1]))
+    sell = ds.engine.sell
+    nnz_local = sell.nnz
+    # parity of this rank's block against the oracle with the full x
+    parity = None
+    if not args.skip_parity:
+        import oracle
+        ds.step()
+        torch.cuda.synchronize()
+        o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, C, sigma)
+        y_ref = oracle.spmv_sell(o, x_all, threads=max(1, (os.cpu_count() or 8) // world))
+        parity = bool(ds.y.cpu().numpy().tobytes() == y_ref.tobytes())
+    for _ in range(args.warmup):
+        ds.step()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    st = torch.cuda.current_stream(device)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = ds.engine.launches
+    sampler = args.clock_sampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.25)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        ds.step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    clk = sampler.stop() if sampler else None
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    nz_t = torch.tensor([nnz_local], dtype=torch.float64, device=device)
+    tdist.all_reduce(nz_t)
+    par_t = torch.tensor([1.0 if parity in (True, None) else 0.0], device=device)
+    tdist.all_reduce(par_t, op=tdist.ReduceOp.MIN)
+    launches = ds.engine.launches - launches0
+
+    # e2e through host buffers: each rank's x slice H2D from pinned memory,
+    # the distributed product, y slice D2H into pinned memory, every step
+    xh = torch.from_numpy(x_all[ds.r0:ds.r1].copy()).pin_memory()
+    yh = torch.empty(ds.y.numel(), dtype=ds.y.dtype).pin_memory()
+    e2e_steps = max(3, min(args.steps, 200))
+    for _ in range(3):
+        ds.x_local.copy_(xh, non_blocking=True)
+        ds.step()
+        yh.copy_(ds.y, non_blocking=True)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ds.x_local.copy_(xh, non_blocking=True)
+        ds.step()
+        yh.copy_(ds.y, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64,
+                         device=device)
+    tdist.all_reduce(e2e_s, op=tdist.ReduceOp.MAX)
+    if rank == 0:
+        ms_max = float(t.item())
+        nnz_tot = float(nz_t.item())
+        value = 2.0 * nnz_tot * args.steps / (ms_max / 1e3) / 1e9
+        v_alg = algorithmic_bytes(nnz_local, crs.n_cols, sell.n_rows_padded, sell.n_chunks)
+        # x read once per rank means the owned slice + halo, not the global n_cols
+        v_alg = v_alg - 8 * crs.n_cols + 8 * (crs.n_rows + ds.plan.halo_entries())
+        per_step_ms = ms_max / args.steps
+        line = {
+            "metric": "spMVM GFLOP/s (2*nnz/t), fp64 SELL-C-sigma", "value": round(value, 3),
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(per_step_ms, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"3D 27-point stencil 128x128x{nz} row-partitioned into "
+                                   f"{world} z-slabs, SELL-32-{sigma}, NCCL halo",
+                       "parallelism": f"row-blocks x{world}", "nnz": int(nnz_tot),
+                       "halo_bytes_per_rank": ds.plan.bytes_per_step(),
+                       "interior_ranges": len(ds.interior),
+                       "boundary_ranges": len(ds.boundary), "build_s": round(build_s, 3),
+                       "parity_vs_oracle_all_ranks": bool(par_t.item() == 1.0),
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": round(v_alg / (per_step_ms / 1e3) / 1e9, 2),
+                         "peak": args.peak, "unit": "GB/s",
+                         "frac": round(v_alg / (per_step_ms / 1e3) / 1e9 / args.peak, 4),
+                         "traffic": None, "bytes_alg_per_launch": v_alg,
+                         "note": "per GPU, step time = max over ranks incl. exchange"},
+            "e2e": {"value": round(2.0 * nnz_tot / float(e2e_s.item()) / 1e9, 3),
+                    "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(8 * crs.n_rows * world),
+                    "d2h_bytes_per_step": int(8 * sell.n_rows_padded * world),
+                    "note": "per-rank pinned x slice in / y slice out each step, max over ranks"},
+            "cpu_baseline": None,
+            "clocks": clk,
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    tdist.destroy_process_group()
+    return 0

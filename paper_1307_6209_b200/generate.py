@@ -101,15 +101,18 @@ def gen_skewed(n, base_len, spike_len, spike_count, seed=0):
 # BASELINE configurations (CRS directly)
 # ---------------------------------------------------------------------------
 
-def _stencil(shape, offsets, diag, off):
+def _stencil(shape, offsets, diag, off, rows=None):
     """CRS of a constant-coefficient stencil on a row-major grid with
     Dirichlet truncation.  Offsets are visited in increasing linear offset,
-    so columns ascend inside every row."""
+    so columns ascend inside every row.  ``rows=(r0, r1)`` builds only that
+    row block (global column indices), for the row-partitioned runs."""
     shape = tuple(int(s) for s in shape)
-    n = int(np.prod(shape))
+    n_glob = int(np.prod(shape))
+    r0, r1 = (0, n_glob) if rows is None else (int(rows[0]), int(rows[1]))
+    n = r1 - r0
     strides = np.cumprod((1,) + shape[::-1][:-1])[::-1]
     offsets = sorted(offsets, key=lambda o: int(np.dot(o, strides)))
-    coords = np.indices(shape).reshape(len(shape), n).astype(np.int32)
+    coords = np.array(np.unravel_index(np.arange(r0, r1), shape), dtype=np.int32)
     k = len(offsets)
     mask = np.ones((n, k), dtype=bool)
     lin = np.empty(k, dtype=np.int64)
@@ -123,10 +126,10 @@ def _stencil(shape, offsets, diag, off):
     rpt = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(counts, out=rpt[1:])
     rr, tt = np.nonzero(mask)
-    col = (rr + lin[tt]).astype(np.int32)
+    col = (rr + r0 + lin[tt]).astype(np.int32)
     is_diag = lin[tt] == 0
     val = np.where(is_diag, diag, off).astype(np.float64)
-    return CRSMatrix(n, n, rpt, col, val)
+    return CRSMatrix(n, n_glob, rpt, col, val)
 
 
 def laplace2d(nx=1000):
@@ -141,6 +144,13 @@ def stencil27(n=128, nz=None):
     nz = n if nz is None else nz
     offs = [(a, b, c) for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)]
     return _stencil((nz, n, n), offs, 26.0, -1.0)
+
+
+def stencil27_slab(n, nz_total, z0, z1):
+    """Rows of z-planes [z0, z1) of the 27-point stencil on n x n x nz_total,
+    with global column indices (one GPU's block of the weak-scaling run)."""
+    offs = [(a, b, c) for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)]
+    return _stencil((nz_total, n, n), offs, 26.0, -1.0, rows=(z0 * n * n, z1 * n * n))
 
 
 def _splitmix64(z):

@@ -1,0 +1,89 @@
+"""The row-partitioned path's CUDA pieces on ONE GPU: every virtual rank's
+block is built and multiplied by its own CudaEngine; the halo exchange is a
+loopback (device copies in one process, no rank waits on another).  Each
+block's y must equal the single-GPU product bit for bit."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1307_6209_b200 as sb
+from paper_1307_6209_b200 import CRSMatrix, dist, generate
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not sb.HAS_CUDA:
+        pytest.skip("no CUDA device")
+
+
+def block(m, r0, r1):
+    s, e = m.rpt[r0], m.rpt[r1]
+    return CRSMatrix(r1 - r0, m.n_cols, m.rpt[r0:r1 + 1] - s, m.col[s:e], m.val[s:e])
+
+
+def virtual_cluster(m, world, C, sigma):
+    dev = torch.device("cuda", 0)
+    bounds = dist.partition_rows(m.rpt, world, C, sigma)
+    blocks = [block(m, int(bounds[r]), int(bounds[r + 1])) for r in range(world)]
+    make = dist.cuda_engine_factory(C, sigma, dev)
+    built = [make(b) for b in blocks]
+    gathered = [(dist.HaloPlan.requests(b.col, bounds, r), built[r][1]["has_padding"])
+                for r, b in enumerate(blocks)]
+    dss = [dist.setup(b, bounds, C, sigma, r, world, dev, None,
+                      plan=dist.HaloPlan.from_requests(r, world, bounds, gathered),
+                      built=built[r]) for r, b in enumerate(blocks)]
+    return bounds, dss
+
+
+def loopback_step(dss, x):
+    xt = torch.from_numpy(x).cuda()
+    for ds in dss:
+        ds.x_local.copy_(xt[ds.r0:ds.r1])
+    for r, ds in enumerate(dss):
+        for p, buf, gidx in ds.send_ops:
+            if gidx is not None:
+                ds.engine.gather(ds.x_full, gidx, buf)
+            dst = [ro for ro in dss[p].recv_ops if ro[0] == r][0][1]
+            dst.copy_(buf)
+        for p in ds.x0_peers:
+            dss[p].x0_buf.copy_(ds.x_full[0:1])
+    for ds in dss:
+        ds.engine.run_ranges(ds.interior, ds.x_full, ds.y)
+        for p, buf, gidx in ds.recv_ops:
+            if gidx is not None:
+                ds.engine.scatter(buf, gidx, ds.x_full)
+        ds.engine.run_ranges(ds.boundary, ds.x_full, ds.y)
+        if ds.x0_recv and ds.has_padding:
+            ds.engine.pad_fixup(ds.x0_buf, ds.y)
+    torch.cuda.synchronize()
+    return [ds.y.cpu().numpy() for ds in dss]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name,C,sigma", [("stencil", 32, 1), ("powerlaw", 32, 128),
+                                          ("hamiltonian", 32, 1)])
+def test_blocks_equal_single_gpu(world, name, C, sigma):
+    m = {"stencil": lambda: generate.stencil27(32, nz=64),
+         "powerlaw": lambda: generate.powerlaw(200_000, seed=4, band=5000),
+         "hamiltonian": lambda: generate.hamiltonian(1 << 18)}[name]()
+    bounds, dss = virtual_cluster(m, world, C, sigma)
+    for x0 in (None, np.inf):
+        x = generate.rhs(m.n_cols)
+        if x0 is not None:
+            x[0] = x0
+        ys = loopback_step(dss, x)
+        for r, y in enumerate(ys):
+            r0, r1 = int(bounds[r]), int(bounds[r + 1])
+            ref = sb.spmv_sell(sb.crs_to_sell(block(m, r0, r1), C, sigma), x)
+            if x0 is None:
+                assert y.tobytes() == ref.tobytes(), (r, name)
+            else:
+                np.testing.assert_array_equal(y, ref)
+        if x0 is None:
+            full = sb.spmv_sell(sb.crs_to_sell(m, C, sigma), x)
+            stitched = np.concatenate([ys[r][: int(bounds[r + 1] - bounds[r])]
+                                       for r in range(world)])
+            assert stitched.tobytes() == full[: m.n_rows].tobytes()
