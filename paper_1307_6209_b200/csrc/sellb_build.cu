@@ -17,6 +17,8 @@
 //                         column permutation                  (formats.py:362-377)
 #include <cub/cub.cuh>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -184,6 +186,7 @@ void free_mat_arrays(sellb_mat* m) {
     cudaFree(m->rl);
     cudaFree(m->perm);
     cudaFree(m->order);
+    cudaFree(m->long_rows);
     cudaFree(m->x_buf);
     cudaFree(m->y_buf);
 }
@@ -233,6 +236,35 @@ int choose_variant(sellb_mat* m, cudaStream_t st, double* beta_eff_out, int64_t*
     }
     if (m->variant == SELLB_VARIANT_AUTO || m->variant == 0)
         m->variant = bytes_skip < bytes_incl ? SELLB_VARIANT_PAD_SKIP : SELLB_VARIANT_PAD_INCL;
+    return 0;
+}
+
+// Rows longer than the threshold go to the kernel's warp-per-row role.
+// Default threshold 64 slots (SELLB_LONG_TH overrides; <= 0 disables).
+int build_long_rows(sellb_mat* m, cudaStream_t st) {
+    cudaFree(m->long_rows);
+    m->long_rows = nullptr;
+    m->n_long = 0;
+    m->long_th = 0x7fffffff;
+    if (!m->rl || m->n_pad == 0) return 0;
+    int th = 64;
+    if (const char* e = getenv("SELLB_LONG_TH")) th = atoi(e);
+    if (th <= 0 || m->max_cl <= th) return 0;
+    std::vector<int32_t> h_rl(m->n_pad);
+    SELLB_CU(cudaMemcpyAsync(h_rl.data(), m->rl, m->n_pad * 4, cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    std::vector<int32_t> rows;
+    for (int64_t p = 0; p < m->n_pad; ++p)
+        if (h_rl[p] > th) rows.push_back((int32_t)p);
+    if (rows.empty()) return 0;
+    std::stable_sort(rows.begin(), rows.end(),
+                     [&](int32_t a, int32_t b) { return h_rl[a] > h_rl[b]; });
+    if (int rc = alloc_dev((void**)&m->long_rows, rows.size() * 4)) return rc;
+    SELLB_CU(cudaMemcpyAsync(m->long_rows, rows.data(), rows.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    m->n_long = (int64_t)rows.size();
+    m->long_th = th;
     return 0;
 }
 
@@ -455,6 +487,7 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     }
     if (int rc = check_stream_error()) return rc;
     if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
+    if (int rc = build_long_rows(m, st)) return rc;
     SELLB_CU(cudaStreamSynchronize(st));
     holder.m = nullptr;
     *out = m;
@@ -547,6 +580,7 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
         m->nnz = s;
         m->variant = SELLB_VARIANT_AUTO;
         if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
+        if (int rc = build_long_rows(m, st)) return rc;
     } else {
         m->nnz = -1;   // unknown without row_lengths
         m->variant = SELLB_VARIANT_PAD_INCL;

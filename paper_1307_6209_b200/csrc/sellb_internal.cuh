@@ -38,6 +38,11 @@ struct sellb_mat {
     int32_t* rl = nullptr;
     int32_t* perm = nullptr;
     int32_t* order = nullptr;
+    // stored rows longer than long_th, longest first: the SpMV kernel's
+    // warp-per-row role (lanes over slots) takes them
+    int32_t* long_rows = nullptr;
+    int64_t n_long = 0;
+    int32_t long_th = 0x7fffffff;
     // end-to-end staging (device x / y for sellb_spmv_host)
     void* x_buf = nullptr;
     void* y_buf = nullptr;

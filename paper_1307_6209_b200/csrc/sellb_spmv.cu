@@ -84,24 +84,115 @@ __device__ __forceinline__ float ld_x(const float* p, uint64_t pol) {
 
 constexpr int kThreads = 256;
 
-// One thread per stored row p in [p0, p1).  CC > 0: compile-time chunk height.
-// ORD 0: y[p] in stored order; ORD 1: y[order[p]] for real rows (fused unpermute).
+template <typename T, bool ACC, int ORD>
+__device__ __forceinline__ void store_row(T* __restrict__ y, const int32_t* __restrict__ order,
+                                          int64_t p, int64_t n_rows, T sum) {
+    if (ORD == 0) {
+        T out = ACC ? Arith<T>::add(y[p], sum) : sum;
+        __stcs(y + p, out);
+    } else if (p < n_rows) {
+        const int64_t o = order[p];
+        y[o] = ACC ? Arith<T>::add(y[o], sum) : sum;
+    }
+}
+
+// Long-row role: one WARP per stored row longer than long_th, lanes over
+// slots (lane l loads slot j0+l; stride C).  The rounded products are formed
+// in parallel, then summed in slot order through warp shuffles -- the same
+// sequence of roundings as the reference's per-row loop, so the result is
+// bitwise identical.  kSeg segments (kSeg*32 slots) are loaded per batch.
+template <typename T, bool ACC, int ORD>
+__device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
+                                         const int32_t* __restrict__ cl,
+                                         const int32_t* __restrict__ rl,
+                                         const int32_t* __restrict__ col,
+                                         const T* __restrict__ val, const T* __restrict__ x,
+                                         T* __restrict__ y, const int32_t* __restrict__ order,
+                                         int64_t C, int64_t p, int64_t n_rows, int lane,
+                                         uint64_t pol_s, uint64_t pol_x) {
+    constexpr int kSeg = 4;
+    const int64_t chunk = p / C;
+    const int64_t base = cs[chunk] + (p - chunk * C);
+    const int w = cl[chunk];
+    const int len = rl[p];
+    const T* vp = val + base;
+    const int32_t* cp = col + base;
+    T sum = T(0);
+    for (int j0 = 0; j0 < len; j0 += 32 * kSeg) {
+        T prod[kSeg];
+        int32_t c[kSeg];
+        T v[kSeg];
+#pragma unroll
+        for (int s = 0; s < kSeg; ++s) {
+            const int j = j0 + s * 32 + lane;
+            v[s] = T(0);
+            c[s] = 0;
+            if (j < len) {
+                v[s] = ld_stream(vp + (int64_t)j * C, pol_s);
+                c[s] = ld_stream(cp + (int64_t)j * C, pol_s);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < kSeg; ++s) {
+            const int j = j0 + s * 32 + lane;
+            prod[s] = (j < len) ? Arith<T>::mul(v[s], ld_x(x + c[s], pol_x)) : T(0);
+        }
+#pragma unroll
+        for (int s = 0; s < kSeg; ++s) {
+            const int rem = len - (j0 + s * 32);          // warp-uniform
+            const int n = rem < 32 ? rem : 32;
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i) {
+                const T q = __shfl_sync(0xffffffffu, prod[s], i);
+                if (i < n) sum = Arith<T>::add(sum, q);
+            }
+        }
+    }
+    if (len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+    if (lane == 0) store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
+}
+
+// The SpMV kernel.  Blocks [0, n_long_blocks) take the long-row role (one
+// warp per row of long_rows[], longest first, so they start early and
+// overlap the bulk); the remaining blocks take one thread per stored row p
+// in [p0, p1) (the paper's GPU design; for C = 32 a warp owns a chunk).
+// CC > 0: compile-time chunk height.  ORD 0: y[p] in stored order; ORD 1:
+// y[order[p]] for real rows (fused unpermute).  In chunks wider than
+// long_th, rows longer than long_th belong to the long-row role and the
+// others stop at their own length (pad-skip semantics).
 template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 8)
 k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
             const int32_t* __restrict__ order, int64_t C_rt, int64_t p0, int64_t p1,
-            int64_t n_rows) {
+            int64_t n_rows, const int32_t* __restrict__ long_rows, int64_t n_long,
+            int long_th) {
     const int64_t C = CC > 0 ? (int64_t)CC : C_rt;
-    const int64_t p = p0 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const int64_t n_long_blocks = (n_long + (kThreads / 32) - 1) / (kThreads / 32);
+    if ((int64_t)blockIdx.x < n_long_blocks) {
+        const int64_t k = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+        if (k >= n_long) return;
+        const int64_t p = long_rows[k];
+        if (p < p0 || p >= p1) return;
+        long_row<T, ACC, ORD>(cs, cl, rl, col, val, x, y, order, C, p, n_rows,
+                              threadIdx.x & 31, pol_s, pol_x);
+        return;
+    }
+    const int64_t p = p0 + ((int64_t)blockIdx.x - n_long_blocks) * kThreads + threadIdx.x;
     if (p >= p1) return;
     const int64_t chunk = p / C;
     const int64_t base = cs[chunk] + (p - chunk * C);
     const int w = cl[chunk];
-    const int len = SKIP ? rl[p] : w;
-    const uint64_t pol_s = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();
+    int len = SKIP ? rl[p] : w;
+    bool skip_pad = SKIP;
+    if (w > long_th) {                   // a chunk holding long rows
+        if (!SKIP) len = rl[p];
+        if (len > long_th) return;       // owned by the long-row role
+        skip_pad = true;
+    }
     const T* vp = val + base;
     const int32_t* cp = col + base;
     T sum = T(0);
@@ -140,15 +231,8 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
         for (int u = 0; u < U; ++u)
             if (j + u < len) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
     }
-    if (SKIP && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
-    if (ORD == 0) {
-        T out = ACC ? Arith<T>::add(y[p], sum) : sum;
-        __stcs(y + p, out);
-    } else if (p < n_rows) {
-        const int64_t o = order[p];
-        T out = ACC ? Arith<T>::add(y[o], sum) : sum;
-        y[o] = out;
-    }
+    if (skip_pad && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+    store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
 }
 
 // Chunk-list variant (multi-GPU interior / boundary passes): block b handles
@@ -235,10 +319,12 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
                cudaStream_t st) {
     const int64_t rows = p1 - p0;
     if (rows <= 0) return 0;
-    const unsigned grid = (unsigned)grid_for(rows, kThreads);
+    const int64_t n_long = m->long_rows ? m->n_long : 0;
+    const int64_t long_blocks = (n_long + kThreads / 32 - 1) / (kThreads / 32);
+    const unsigned grid = (unsigned)(grid_for(rows, kThreads) + long_blocks);
     k_spmv_sell<T, CC, SKIP, ACC, ORD, 4><<<grid, kThreads, 0, st>>>(
         m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0,
-        p1, m->n_rows);
+        p1, m->n_rows, m->long_rows, n_long, n_long ? m->long_th : 0x7fffffff);
     return 0;
 }
 
