@@ -160,7 +160,7 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
 // y[order[p]] for real rows (fused unpermute).  In chunks wider than
 // long_th, rows longer than long_th belong to the long-row role and the
 // others stop at their own length (pad-skip semantics).
-template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U>
+template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U, bool LONG>
 __global__ void __launch_bounds__(kThreads, 8)
 k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
@@ -171,8 +171,8 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     const int64_t C = CC > 0 ? (int64_t)CC : C_rt;
     const uint64_t pol_s = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
-    const int64_t n_long_blocks = (n_long + (kThreads / 32) - 1) / (kThreads / 32);
-    if ((int64_t)blockIdx.x < n_long_blocks) {
+    const int64_t n_long_blocks = LONG ? (n_long + (kThreads / 32) - 1) / (kThreads / 32) : 0;
+    if (LONG && (int64_t)blockIdx.x < n_long_blocks) {
         const int64_t k = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
         if (k >= n_long) return;
         const int64_t p = long_rows[k];
@@ -188,7 +188,7 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     const int w = cl[chunk];
     int len = SKIP ? rl[p] : w;
     bool skip_pad = SKIP;
-    if (w > long_th) {                   // a chunk holding long rows
+    if (LONG && w > long_th) {           // a chunk holding long rows
         if (!SKIP) len = rl[p];
         if (len > long_th) return;       // owned by the long-row role
         skip_pad = true;
@@ -322,9 +322,14 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     const int64_t n_long = m->long_rows ? m->n_long : 0;
     const int64_t long_blocks = (n_long + kThreads / 32 - 1) / (kThreads / 32);
     const unsigned grid = (unsigned)(grid_for(rows, kThreads) + long_blocks);
-    k_spmv_sell<T, CC, SKIP, ACC, ORD, 4><<<grid, kThreads, 0, st>>>(
-        m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0,
-        p1, m->n_rows, m->long_rows, n_long, n_long ? m->long_th : 0x7fffffff);
+    if (n_long)
+        k_spmv_sell<T, CC, SKIP, ACC, ORD, 4, true><<<grid, kThreads, 0, st>>>(
+            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,
+            p0, p1, m->n_rows, m->long_rows, n_long, m->long_th);
+    else
+        k_spmv_sell<T, CC, SKIP, ACC, ORD, 4, false><<<grid, kThreads, 0, st>>>(
+            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,
+            p0, p1, m->n_rows, nullptr, 0, 0x7fffffff);
     return 0;
 }
 
