@@ -13,7 +13,7 @@ from .errors import (DimensionError, ParameterError, ResourceError,
                      StructuralError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsellb200.so")
+LIB_PATH = os.environ.get("SELLB_LIB_PATH") or os.path.join(HERE, "libsellb200.so")
 
 SELLB_F64 = 0
 SELLB_F32 = 1
@@ -117,6 +117,8 @@ def load():
             except OSError as exc:
                 raise ResourceError(f"cannot load {LIB_PATH}: {exc}") from exc
             for name, (res, args) in _PROTOS.items():
+                if not hasattr(lib, name):      # older builds under SELLB_LIB_PATH
+                    continue
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -240,14 +240,14 @@ int choose_variant(sellb_mat* m, cudaStream_t st, double* beta_eff_out, int64_t*
 }
 
 // Rows longer than the threshold go to the kernel's warp-per-row role.
-// Default threshold 64 slots (SELLB_LONG_TH overrides; <= 0 disables).
+// Default threshold 256 slots (SELLB_LONG_TH overrides; <= 0 disables).
 int build_long_rows(sellb_mat* m, cudaStream_t st) {
     cudaFree(m->long_rows);
     m->long_rows = nullptr;
     m->n_long = 0;
     m->long_th = 0x7fffffff;
     if (!m->rl || m->n_pad == 0) return 0;
-    int th = 64;
+    int th = 256;
     if (const char* e = getenv("SELLB_LONG_TH")) th = atoi(e);
     if (th <= 0 || m->max_cl <= th) return 0;
     std::vector<int32_t> h_rl(m->n_pad);
