@@ -261,6 +261,93 @@ def load_profile_traffic(key):
     return None if v is None else float(v)
 
 
+ARRAYS = ("cs", "cl", "col", "val", "perm", "row_lengths")
+
+
+def host_workload(args, dt_np):
+    """cfg1-cfg4: CRS generated on the host, built on the GPU."""
+    import torch
+    import oracle
+    import paper_1307_6209_b200 as sb
+    crs, desc = make_matrix(args.config)
+    x = np.random.default_rng(12345).uniform(-1, 1, crs.n_cols).astype(dt_np)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = sb.crs_to_sell(crs, 32, args.sigma, dtype=dt_np)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+
+    def parity(yd):
+        o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val.astype(dt_np), crs.n_rows,
+                               crs.n_cols, 32, args.sigma)
+        y_ref = oracle.spmv_sell(o, x, threads=os.cpu_count() or 1)
+        ok = yd.cpu().numpy().tobytes() == y_ref.tobytes()
+        return ok and all(getattr(s, k).tobytes() == getattr(o, k).tobytes() for k in ARRAYS)
+
+    def cpu(budget):
+        o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, 32,
+                               args.sigma)
+        gf, kind, cores, sample, _ = cpu_reference_run(o, x.astype(np.float64),
+                                                       budget_s=budget)
+        return {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": kind,
+                "sample": sample + f"; host {host_cpu_desc()}"}
+
+    return {"sell": s, "desc": desc, "x": x, "build_s": build_s, "parity": parity, "cpu": cpu}
+
+
+def cfg5_workload(args, dt_np):
+    """cfg5: the N = 2^26, ~1.3e9-nonzero banded-random matrix generated and
+    built on the GPU (16 GB of CRS never touches the host).  Parity and the
+    CPU baseline use row blocks regenerated on the host (row-addressable
+    generator; block builds equal slices of the global build)."""
+    import torch
+    import oracle
+    import paper_1307_6209_b200 as sb
+    from paper_1307_6209_b200 import CRSMatrix, generate
+    n = args.n or (1 << 26)
+    sigma = args.sigma
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rpt, col, val = generate.hamiltonian_device(n, device=0, dtype=dt_np)
+    t_gen = time.perf_counter() - t0
+    s = sb.crs_to_sell_device(rpt, col, val, n, n, 32, sigma)
+    del rpt, col, val
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    build_s = time.perf_counter() - t0 - t_gen
+    x = np.random.default_rng(12345).uniform(-1, 1, n).astype(dt_np)
+    blk = 1 << 16
+
+    def block(r0, r1):
+        rp, cl_, vl = generate.hamiltonian_rows(n, r0, r1)
+        return CRSMatrix(r1 - r0, n, rp, cl_, vl.astype(dt_np) if dt_np == np.float32 else vl)
+
+    def parity(yd):
+        ok = True
+        for r0 in (0, (n // 2) // blk * blk, n - blk):
+            b = block(r0, r0 + blk)
+            o = oracle.crs_to_sell(b.rpt, b.col, b.val, b.n_rows, n, 32, sigma)
+            got = s.export_range(r0 // 32, (r0 + blk) // 32)
+            for k in ("cs", "cl", "col", "val", "row_lengths"):
+                ok = ok and got[k].tobytes() == getattr(o, k).tobytes()
+            y_ref = oracle.spmv_sell(o, x)
+            ok = ok and yd[r0:r0 + blk].cpu().numpy().tobytes() == y_ref.tobytes()
+        return ok
+
+    def cpu(budget):
+        b = block(0, min(n, 1 << 20))
+        o = oracle.crs_to_sell(b.rpt, b.col, b.val.astype(np.float64), b.n_rows, n, 32, sigma)
+        gf, kind, cores, sample, _ = cpu_reference_run(o, x.astype(np.float64),
+                                                       budget_s=budget)
+        return {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": kind,
+                "sample": f"rows [0, {b.n_rows}) block of the N={n} matrix: " + sample
+                          + f"; host {host_cpu_desc()}"}
+
+    return {"sell": s, "desc": f"banded-random Hamiltonian-like N={n} (device-generated, "
+                               f"generation {t_gen:.2f} s)",
+            "x": x, "build_s": build_s, "parity": parity, "cpu": cpu}
+
+
 def run_ours(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -276,21 +363,16 @@ def run_ours(args):
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    crs, desc = make_matrix(args.config)
     dt_np = np.float32 if args.dtype == "f32" else np.float64
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     sigma = args.sigma
-    x_host = np.random.default_rng(12345).uniform(-1, 1, crs.n_cols).astype(dt_np)
-
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    s = sb.crs_to_sell(crs, 32, sigma, dtype=dt_np)
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t0
+    wl = (cfg5_workload if args.config == "cfg5" else host_workload)(args, dt_np)
+    s, desc, x_host, build_s = wl["sell"], wl["desc"], wl["x"], wl["build_s"]
     info = s.info()
+    n_rows, n_cols = info.n_rows, info.n_cols
     nnz, n_pad, n_chunks, slots = info.nnz, info.n_rows_padded, info.n_chunks, info.slots
     s_v = 4 if args.dtype == "f32" else 8
-    v_alg = algorithmic_bytes(nnz, crs.n_cols, n_pad, n_chunks, s_v=s_v)
+    v_alg = algorithmic_bytes(nnz, n_cols, n_pad, n_chunks, s_v=s_v)
     lib = _lib.load()
     handle = s.handle
 
@@ -308,13 +390,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     parity = None
     if not args.skip_parity:
-        o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val.astype(dt_np), crs.n_rows,
-                               crs.n_cols, 32, sigma)
-        y_ref = oracle.spmv_sell(o, x_host, threads=os.cpu_count() or 1)
-        parity = bool(yd.cpu().numpy().tobytes() == y_ref.tobytes())
-        arrays_ok = all(getattr(s, k).tobytes() == getattr(o, k).tobytes()
-                        for k in ("cs", "cl", "col", "val", "perm", "row_lengths"))
-        parity = parity and arrays_ok
+        parity = bool(wl["parity"](yd))
         if not parity:
             log("PARITY FAILURE against the oracle")
 
@@ -359,9 +435,9 @@ def run_ours(args):
     # e2e: the public host-array API (sellb_spmv_host) with pinned x / y
     import ctypes
     px, py = ctypes.c_void_p(), ctypes.c_void_p()
-    _lib.check(lib.sellb_host_alloc(crs.n_cols * s_v, ctypes.byref(px)))
+    _lib.check(lib.sellb_host_alloc(n_cols * s_v, ctypes.byref(px)))
     _lib.check(lib.sellb_host_alloc(n_pad * s_v, ctypes.byref(py)))
-    xh = np.ctypeslib.as_array((ctypes.c_byte * (crs.n_cols * s_v)).from_address(px.value)).view(dt_np)
+    xh = np.ctypeslib.as_array((ctypes.c_byte * (n_cols * s_v)).from_address(px.value)).view(dt_np)
     yh = np.ctypeslib.as_array((ctypes.c_byte * (n_pad * s_v)).from_address(py.value)).view(dt_np)
     xh[:] = x_host
     e2e_steps = max(3, min(args.steps, 200))
@@ -379,12 +455,7 @@ def run_ours(args):
     # reference CPU path on this host, bounded sample (rank 0, N=1)
     cpu = None
     if not args.skip_cpu:
-        o_cpu = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, 32,
-                                   sigma)
-        gf, kind, cores, sample, _ = cpu_reference_run(o_cpu, x_host.astype(np.float64),
-                                                       budget_s=args.cpu_budget)
-        cpu = {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": sample + f"; host {host_cpu_desc()}"}
+        cpu = wl["cpu"](args.cpu_budget)
 
     traffic = load_profile_traffic(f"{args.config}_s{sigma}_{args.dtype}")
     line = {
@@ -393,7 +464,7 @@ def run_ours(args):
         "ms_per_step": round(step_ms, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": f"{desc}, SELL-32-{sigma}", "C": 32, "sigma": sigma,
-                   "n_rows": crs.n_rows, "nnz": nnz, "slots": slots,
+                   "n_rows": n_rows, "nnz": nnz, "slots": slots,
                    "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
                    "l2": ("flushed between steps (%d MB scratch write); value from the "
                           "SpMV's own events" % (4 * l2_bytes // 2**20)) if flush is not None
@@ -406,7 +477,7 @@ def run_ours(args):
                      "bytes_alg_per_launch": v_alg,
                      "kernel_ms": round(kern_ms, 5)},
         "e2e": {"value": round(2.0 * nnz / e2e_s / 1e9, 3), "unit": UNIT,
-                "h2d_bytes_per_step": crs.n_cols * s_v, "d2h_bytes_per_step": n_pad * s_v,
+                "h2d_bytes_per_step": n_cols * s_v, "d2h_bytes_per_step": n_pad * s_v,
                 "ms_per_step": round(e2e_s * 1e3, 4), "api": "sellb_spmv_host (pinned)",
                 "matches_device": e2e_ok},
         "cpu_baseline": cpu,
@@ -429,6 +500,7 @@ def main(argv=None):
     ap.add_argument("--skip-parity", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--n", type=int, default=0, help="cfg5 rows (default 2^26)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

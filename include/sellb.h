@@ -116,6 +116,13 @@ int sellb_export(const sellb_mat* m, int64_t* cs, int32_t* cl, int32_t* col,
                  void* val, int32_t* perm, int32_t* row_lengths, void* stream,
                  int32_t ptrs_on_device);
 
+/* Copy the arrays of chunks [c0, c1) out (host destination): cs is rebased
+ * to start at 0 (c1-c0+1 entries), col/val cover cs[c0]..cs[c1), row_lengths
+ * cover stored rows [c0*C, c1*C).  Block-wise parity at sizes the host
+ * cannot hold whole (cfg5). */
+int sellb_export_range(const sellb_mat* m, int64_t c0, int64_t c1, int64_t* cs, int32_t* cl,
+                       int32_t* col, void* val, int32_t* row_lengths);
+
 int sellb_set_variant(sellb_mat* m, int32_t variant);
 void sellb_free(sellb_mat* m);
 
@@ -184,6 +191,16 @@ int sellb_gather(const void* x, const int32_t* idx, void* out, int64_t n, int32_
                  void* stream);
 int sellb_scatter(const void* in, const int32_t* idx, void* x, int64_t n, int32_t dtype,
                   void* stream);
+
+/* cfg5 generator (BASELINE configs[4]) straight into device CRS, rows
+ * [r0, r1) of the N = n banded-random matrix (generate.py:hamiltonian_rows):
+ * first rpt[r1-r0+1] (returns nnz), then col/val into caller buffers. */
+int sellb_gen_hamiltonian_rpt(int64_t n, int64_t r0, int64_t r1, const int64_t* offs_dev,
+                              int32_t n_off, double keep, uint64_t seed, int64_t* rpt_dev,
+                              int64_t* nnz_out, void* stream);
+int sellb_gen_hamiltonian_fill(int64_t n, int64_t r0, int64_t r1, const int64_t* offs_dev,
+                               int32_t n_off, double keep, uint64_t seed, const int64_t* rpt_dev,
+                               int32_t* col_dev, void* val_dev, int32_t dtype, void* stream);
 
 /* Pinned host buffers for the end-to-end path. */
 int sellb_host_alloc(size_t bytes, void** out);

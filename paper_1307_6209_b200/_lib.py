@@ -32,7 +32,8 @@ EXPORTED = (
     "sellb_spmv_crs_range_host", "sellb_spmv_crs", "sellb_chunk_occupancy",
     "sellb_sector_occupancy", "sellb_read_sum", "sellb_copy", "sellb_l2_flush",
     "sellb_host_alloc", "sellb_host_free", "sellb_gather", "sellb_scatter",
-    "sellb_pad_fixup",
+    "sellb_pad_fixup", "sellb_gen_hamiltonian_rpt", "sellb_gen_hamiltonian_fill",
+    "sellb_export_range",
 )
 
 
@@ -91,7 +92,13 @@ _PROTOS = {
     "sellb_gather": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
     "sellb_scatter": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
     "sellb_pad_fixup": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "sellb_gen_hamiltonian_rpt": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i32, ctypes.c_double,
+                                                 ctypes.c_uint64, _vp, ctypes.POINTER(_i64),
+                                                 _vp]),
+    "sellb_gen_hamiltonian_fill": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i32, ctypes.c_double,
+                                                  ctypes.c_uint64, _vp, _vp, _vp, _i32, _vp]),
     "sellb_host_free": (ctypes.c_int, [_vp]),
+    "sellb_export_range": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

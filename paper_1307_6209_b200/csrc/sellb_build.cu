@@ -187,6 +187,16 @@ void free_mat_arrays(sellb_mat* m) {
     cudaFree(m->perm);
     cudaFree(m->order);
     cudaFree(m->long_rows);
+    if (m->pipe_ready) {
+        cudaStreamDestroy(m->s_h2d);
+        cudaStreamDestroy(m->s_comp);
+        cudaStreamDestroy(m->s_d2h);
+        cudaEventDestroy(m->ev_start);
+        for (int i = 0; i < sellb_mat::kPipe; ++i) {
+            cudaEventDestroy(m->ev_x[i]);
+            cudaEventDestroy(m->ev_blk[i]);
+        }
+    }
     cudaFree(m->x_buf);
     cudaFree(m->y_buf);
 }
@@ -630,6 +640,32 @@ int sellb_export(const sellb_mat* m, int64_t* cs, int32_t* cl, int32_t* col, voi
         SELLB_CU(cudaMemcpyAsync(row_lengths, m->rl, m->n_pad * 4, kind, st));
     }
     SELLB_CU(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int sellb_export_range(const sellb_mat* m, int64_t c0, int64_t c1, int64_t* cs, int32_t* cl,
+                       int32_t* col, void* val, int32_t* row_lengths) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    if (c0 < 0 || c1 > m->n_chunks || c0 > c1) return set_error(SELLB_EPARAM, "bad chunk range");
+    DeviceGuard guard(m->device);
+    const int64_t nc = c1 - c0;
+    std::vector<int64_t> hcs(nc + 1);
+    SELLB_CU(cudaMemcpy(hcs.data(), m->cs + c0, (nc + 1) * 8, cudaMemcpyDeviceToHost));
+    const int64_t s0 = hcs[0], s1 = hcs[nc];
+    if (cs)
+        for (int64_t i = 0; i <= nc; ++i) cs[i] = hcs[i] - s0;
+    if (cl && nc) SELLB_CU(cudaMemcpy(cl, m->cl + c0, nc * 4, cudaMemcpyDeviceToHost));
+    if (col && s1 > s0)
+        SELLB_CU(cudaMemcpy(col, m->col + s0, (s1 - s0) * 4, cudaMemcpyDeviceToHost));
+    if (val && s1 > s0)
+        SELLB_CU(cudaMemcpy(val, (const char*)m->val + s0 * vsize(m->dtype),
+                            (s1 - s0) * vsize(m->dtype), cudaMemcpyDeviceToHost));
+    if (row_lengths && nc) {
+        if (!m->rl) return set_error(SELLB_EPARAM, "matrix has no row_lengths");
+        SELLB_CU(cudaMemcpy(row_lengths, m->rl + c0 * m->C, nc * m->C * 4,
+                            cudaMemcpyDeviceToHost));
+    }
     return 0;
 }
 

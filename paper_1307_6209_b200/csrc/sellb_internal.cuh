@@ -47,6 +47,15 @@ struct sellb_mat {
     void* x_buf = nullptr;
     void* y_buf = nullptr;
     std::mutex mu;
+    // pipelined host path: x pieces H2D / row blocks / y pieces D2H overlap
+    static constexpr int kPipe = 16;
+    bool pipe_ready = false;
+    cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_x[kPipe] = {}, ev_blk[kPipe] = {};
+    int n_pieces = 0;
+    int64_t x_off[kPipe + 1] = {};        // column boundaries of the x pieces
+    int64_t blk_c[kPipe + 1] = {};        // chunk boundaries of the row blocks
+    int blk_need[kPipe] = {};             // last x piece a row block reads
 };
 
 namespace sellb {

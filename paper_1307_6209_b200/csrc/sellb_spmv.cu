@@ -25,7 +25,10 @@
 // non-finite x[0] it turns the row into NaN.  One fused fix-up
 // (sum += 0 * x[0] when the row has padding) reproduces that exactly, so both
 // variants are bit-identical to the reference for every input.
+#include <stdlib.h>
+
 #include <algorithm>
+#include <vector>
 
 #include "sellb_internal.cuh"
 
@@ -464,6 +467,106 @@ int sellb_pad_fixup(const sellb_mat* m, const void* x0, void* y, void* stream) {
     return 0;
 }
 
+}  // extern "C"
+
+namespace {
+
+// per-chunk maximum column index (real slots and padding alike; padding
+// holds column 0 so it never raises the maximum)
+__global__ void k_chunk_maxcol(const int64_t* __restrict__ cs, const int32_t* __restrict__ col,
+                               int64_t n_chunks, int32_t* __restrict__ out) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= n_chunks) return;
+    int32_t mx = 0;
+    for (int64_t k = cs[w] + lane; k < cs[w + 1]; k += 32) mx = max(mx, col[k]);
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) out[w] = mx;
+}
+
+// One-time setup of the pipelined host path: row blocks of equal chunk
+// count, x pieces of equal column count, and for every row block the last x
+// piece its columns reach (so its kernel can start as soon as that piece has
+// landed).
+int pipe_setup(sellb_mat* m) {
+    if (m->pipe_ready) return 0;
+    const int P = (int)std::min<int64_t>(sellb_mat::kPipe, std::max<int64_t>(m->n_chunks, 1));
+    std::vector<int32_t> maxcol(std::max<int64_t>(m->n_chunks, 1), 0);
+    if (m->n_chunks) {
+        int32_t* d = nullptr;
+        SELLB_CU(cudaMalloc(&d, m->n_chunks * 4));
+        k_chunk_maxcol<<<(unsigned)grid_for(m->n_chunks * 32, kThreads), kThreads>>>(
+            m->cs, m->col, m->n_chunks, d);
+        cudaError_t e = cudaMemcpy(maxcol.data(), d, m->n_chunks * 4, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        SELLB_CU(e);
+    }
+    m->n_pieces = P;
+    for (int i = 0; i <= P; ++i) {
+        m->x_off[i] = m->n_cols * i / P;
+        m->blk_c[i] = m->n_chunks * i / P;
+    }
+    for (int b = 0; b < P; ++b) {
+        int32_t mx = 0;
+        for (int64_t c = m->blk_c[b]; c < m->blk_c[b + 1]; ++c) mx = std::max(mx, maxcol[c]);
+        int k = 0;
+        while (k + 1 < P && m->x_off[k + 1] <= mx) ++k;
+        m->blk_need[b] = k;
+    }
+    SELLB_CU(cudaStreamCreateWithFlags(&m->s_h2d, cudaStreamNonBlocking));
+    SELLB_CU(cudaStreamCreateWithFlags(&m->s_comp, cudaStreamNonBlocking));
+    SELLB_CU(cudaStreamCreateWithFlags(&m->s_d2h, cudaStreamNonBlocking));
+    SELLB_CU(cudaEventCreateWithFlags(&m->ev_start, cudaEventDisableTiming));
+    for (int i = 0; i < sellb_mat::kPipe; ++i) {
+        SELLB_CU(cudaEventCreateWithFlags(&m->ev_x[i], cudaEventDisableTiming));
+        SELLB_CU(cudaEventCreateWithFlags(&m->ev_blk[i], cudaEventDisableTiming));
+    }
+    m->pipe_ready = true;
+    return 0;
+}
+
+// y = A x with host x / y: x streams in column pieces on one copy engine,
+// row blocks start as soon as the x they read has landed, and each block's
+// y streams back on the other copy engine while later blocks compute.
+int spmv_host_pipelined(sellb_mat* m, const void* x_host, void* y_host, cudaStream_t user) {
+    if (int rc = pipe_setup(m)) return rc;
+    const size_t vs = vsize(m->dtype);
+    const int P = m->n_pieces;
+    SELLB_CU(cudaEventRecord(m->ev_start, user));
+    SELLB_CU(cudaStreamWaitEvent(m->s_h2d, m->ev_start, 0));
+    SELLB_CU(cudaStreamWaitEvent(m->s_comp, m->ev_start, 0));
+    for (int i = 0; i < P; ++i) {
+        const int64_t a = m->x_off[i], b = m->x_off[i + 1];
+        if (b > a)
+            SELLB_CU(cudaMemcpyAsync((char*)m->x_buf + a * vs, (const char*)x_host + a * vs,
+                                     (b - a) * vs, cudaMemcpyHostToDevice, m->s_h2d));
+        SELLB_CU(cudaEventRecord(m->ev_x[i], m->s_h2d));
+    }
+    int waited = -1;
+    for (int b = 0; b < P; ++b) {
+        if (m->blk_need[b] > waited) {
+            SELLB_CU(cudaStreamWaitEvent(m->s_comp, m->ev_x[m->blk_need[b]], 0));
+            waited = m->blk_need[b];
+        }
+        if (int rc = launch_spmv(m, m->x_buf, m->y_buf, m->blk_c[b], m->blk_c[b + 1], 0,
+                                 SELLB_ORDER_STORED, m->s_comp))
+            return rc;
+        SELLB_CU(cudaEventRecord(m->ev_blk[b], m->s_comp));
+        SELLB_CU(cudaStreamWaitEvent(m->s_d2h, m->ev_blk[b], 0));
+        const int64_t y0 = m->blk_c[b] * m->C, y1 = m->blk_c[b + 1] * m->C;
+        if (y1 > y0)
+            SELLB_CU(cudaMemcpyAsync((char*)y_host + y0 * vs, (const char*)m->y_buf + y0 * vs,
+                                     (y1 - y0) * vs, cudaMemcpyDeviceToHost, m->s_d2h));
+    }
+    SELLB_CU(cudaStreamSynchronize(m->s_d2h));
+    SELLB_CU(cudaStreamSynchronize(m->s_h2d));
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
 int sellb_spmv_host(sellb_mat* m, const void* x_host, void* y_host, int64_t c0, int64_t c1,
                     int32_t accumulate, int32_t out_order, void* stream) {
     clear_error();
@@ -477,6 +580,9 @@ int sellb_spmv_host(sellb_mat* m, const void* x_host, void* y_host, int64_t c0, 
     const int64_t ny = out_order == SELLB_ORDER_ORIGINAL ? m->n_rows : m->n_pad;
     if (!m->x_buf) SELLB_CU(cudaMalloc(&m->x_buf, std::max<int64_t>(m->n_cols, 1) * vs));
     if (!m->y_buf) SELLB_CU(cudaMalloc(&m->y_buf, std::max<int64_t>(m->n_pad, 1) * vs));
+    if (!accumulate && out_order == SELLB_ORDER_STORED && c0 == 0 && c1 == m->n_chunks &&
+        m->n_chunks >= 4 * sellb_mat::kPipe && !getenv("SELLB_NO_PIPELINE"))
+        return spmv_host_pipelined(m, x_host, y_host, st);
     if (m->n_cols)
         SELLB_CU(cudaMemcpyAsync(m->x_buf, x_host, m->n_cols * vs, cudaMemcpyHostToDevice, st));
     // rows touched by the range

@@ -306,6 +306,24 @@ class SellMatrix:
         _lib.check(_lib.load().sellb_device_arrays(self.handle, ctypes.byref(d)))
         return {name: getattr(d, name) for name, _ in d._fields_}
 
+    def export_range(self, c0, c1):
+        """Host copies of chunks [c0, c1): cs (rebased), cl, col, val and
+        row_lengths -- block-wise parity without exporting the whole matrix."""
+        info = self.info()
+        c0, c1 = int(c0), int(c1)
+        lib = _lib.load()
+        cs = np.empty(c1 - c0 + 1, OFFSET_DTYPE)
+        _lib.check(lib.sellb_export_range(self.handle, c0, c1, _lib.ptr(cs), None, None,
+                                          None, None))
+        slots = int(cs[-1])
+        out = {"cs": cs, "cl": np.empty(c1 - c0, INDEX_DTYPE),
+               "col": np.empty(slots, INDEX_DTYPE), "val": np.empty(slots, self.dtype),
+               "row_lengths": np.empty((c1 - c0) * int(info.C), INDEX_DTYPE)}
+        _lib.check(lib.sellb_export_range(self.handle, c0, c1, None, _lib.ptr(out["cl"]),
+                                          _lib.ptr(out["col"]), _lib.ptr(out["val"]),
+                                          _lib.ptr(out["row_lengths"])))
+        return out
+
     @property
     def variant(self):
         return {1: "pad_skip", 2: "pad_incl"}.get(self.info().variant, "auto")

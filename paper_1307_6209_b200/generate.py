@@ -226,3 +226,40 @@ CONFIGS = {
 def canonical_crs(coo):
     from .formats import coo_to_crs
     return coo_to_crs(coo)
+
+
+def hamiltonian_offsets(n, offsets=HAM_OFFSETS):
+    """The sorted offset set of hamiltonian_rows (d = 0 plus +-d, |d| < n)."""
+    return np.array(sorted({0} | {d for d in offsets if d < n} | {-d for d in offsets if d < n}),
+                    dtype=np.int64)
+
+
+def hamiltonian_device(n=1 << 26, r0=0, r1=None, keep=0.78, seed=11, device=0,
+                       dtype=np.float64, offsets=HAM_OFFSETS):
+    """Rows [r0, r1) of the cfg5 matrix generated ON the GPU (CUDA kernels in
+    csrc/sellb_gen.cu, bit-identical to hamiltonian_rows).  Returns torch
+    CUDA tensors (rpt int64[rows+1], col int32[nnz], val f64/f32[nnz]) --
+    the 1.3e9-nonzero matrix never exists in host memory."""
+    import ctypes
+    import torch
+    from . import _lib
+    r1 = n if r1 is None else r1
+    lib = _lib.require_device()
+    dev = torch.device("cuda", device)
+    offs = torch.from_numpy(hamiltonian_offsets(n, offsets)).to(dev)
+    rows = r1 - r0
+    rpt = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    nnz = ctypes.c_int64(0)
+    with torch.cuda.device(dev):
+        _lib.check(lib.sellb_gen_hamiltonian_rpt(n, r0, r1, offs.data_ptr(), offs.numel(),
+                                                 keep, seed, rpt.data_ptr(),
+                                                 ctypes.byref(nnz), st))
+        col = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+        f32 = np.dtype(dtype) == np.float32
+        val = torch.empty(max(nnz.value, 1), dtype=torch.float32 if f32 else torch.float64,
+                          device=dev)
+        _lib.check(lib.sellb_gen_hamiltonian_fill(
+            n, r0, r1, offs.data_ptr(), offs.numel(), keep, seed, rpt.data_ptr(),
+            col.data_ptr(), val.data_ptr(), _lib.SELLB_F32 if f32 else _lib.SELLB_F64, st))
+    return rpt, col[: nnz.value], val[: nnz.value]
