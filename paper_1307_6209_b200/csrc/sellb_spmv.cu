@@ -490,7 +490,9 @@ __global__ void k_chunk_maxcol(const int64_t* __restrict__ cs, const int32_t* __
 // landed).
 int pipe_setup(sellb_mat* m) {
     if (m->pipe_ready) return 0;
-    const int P = (int)std::min<int64_t>(sellb_mat::kPipe, std::max<int64_t>(m->n_chunks, 1));
+    int want = 4;   // measured best on cfg2 (tools/e2e_probe.py): 2:0.580 4:0.568 8:0.596 16:0.650 ms
+    if (const char* e = getenv("SELLB_PIPE")) want = std::max(1, std::min(atoi(e), sellb_mat::kPipe));
+    const int P = (int)std::min<int64_t>(want, std::max<int64_t>(m->n_chunks, 1));
     std::vector<int32_t> maxcol(std::max<int64_t>(m->n_chunks, 1), 0);
     if (m->n_chunks) {
         int32_t* d = nullptr;
@@ -501,25 +503,28 @@ int pipe_setup(sellb_mat* m) {
         cudaFree(d);
         SELLB_CU(e);
     }
+    // x piece b ends just past the highest column row block b reads, so block
+    // b can start as soon as piece b has landed (for banded matrices the
+    // pieces then track the row blocks and H2D, compute and D2H overlap)
     m->n_pieces = P;
-    for (int i = 0; i <= P; ++i) {
-        m->x_off[i] = m->n_cols * i / P;
-        m->blk_c[i] = m->n_chunks * i / P;
-    }
+    m->x_off[0] = 0;
     for (int b = 0; b < P; ++b) {
-        int32_t mx = 0;
-        for (int64_t c = m->blk_c[b]; c < m->blk_c[b + 1]; ++c) mx = std::max(mx, maxcol[c]);
-        int k = 0;
-        while (k + 1 < P && m->x_off[k + 1] <= mx) ++k;
-        m->blk_need[b] = k;
+        m->blk_c[b] = m->n_chunks * b / P;
+        m->blk_c[b + 1] = m->n_chunks * (b + 1) / P;
+        int64_t mx = -1;
+        for (int64_t c = m->blk_c[b]; c < m->blk_c[b + 1]; ++c) mx = std::max<int64_t>(mx, maxcol[c]);
+        int64_t end = std::min<int64_t>(std::max<int64_t>(m->x_off[b], mx + 1), m->n_cols);
+        m->x_off[b + 1] = (b + 1 == P) ? m->n_cols : end;
+        m->blk_need[b] = b;
     }
     SELLB_CU(cudaStreamCreateWithFlags(&m->s_h2d, cudaStreamNonBlocking));
     SELLB_CU(cudaStreamCreateWithFlags(&m->s_comp, cudaStreamNonBlocking));
     SELLB_CU(cudaStreamCreateWithFlags(&m->s_d2h, cudaStreamNonBlocking));
-    SELLB_CU(cudaEventCreateWithFlags(&m->ev_start, cudaEventDisableTiming));
+    const unsigned evf = getenv("SELLB_PIPE_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+    SELLB_CU(cudaEventCreateWithFlags(&m->ev_start, evf));
     for (int i = 0; i < sellb_mat::kPipe; ++i) {
-        SELLB_CU(cudaEventCreateWithFlags(&m->ev_x[i], cudaEventDisableTiming));
-        SELLB_CU(cudaEventCreateWithFlags(&m->ev_blk[i], cudaEventDisableTiming));
+        SELLB_CU(cudaEventCreateWithFlags(&m->ev_x[i], evf));
+        SELLB_CU(cudaEventCreateWithFlags(&m->ev_blk[i], evf));
     }
     m->pipe_ready = true;
     return 0;
@@ -560,6 +565,20 @@ int spmv_host_pipelined(sellb_mat* m, const void* x_host, void* y_host, cudaStre
     }
     SELLB_CU(cudaStreamSynchronize(m->s_d2h));
     SELLB_CU(cudaStreamSynchronize(m->s_h2d));
+    if (getenv("SELLB_PIPE_TRACE")) {        // debug timeline (events carry timing)
+        float t;
+        fprintf(stderr, "pipe x:");
+        for (int i = 0; i < P; ++i) {
+            cudaEventElapsedTime(&t, m->ev_start, m->ev_x[i]);
+            fprintf(stderr, " %.3f", t);
+        }
+        fprintf(stderr, "\npipe k:");
+        for (int i = 0; i < P; ++i) {
+            cudaEventElapsedTime(&t, m->ev_start, m->ev_blk[i]);
+            fprintf(stderr, " %.3f", t);
+        }
+        fprintf(stderr, "\n");
+    }
     return 0;
 }
 
