@@ -56,6 +56,16 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// kind: 0 evict_first, 1 evict_normal, 2 evict_last
+__device__ __forceinline__ uint64_t make_policy(int kind) {
+    return kind == 0 ? policy_evict_first() : kind == 1 ? policy_evict_normal()
+                                                         : policy_evict_last();
+}
 
 // streaming (read-once) loads of the matrix arrays
 __device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
@@ -170,10 +180,10 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
             const int32_t* __restrict__ order, int64_t C_rt, int64_t p0, int64_t p1,
             int64_t n_rows, const int32_t* __restrict__ long_rows, int64_t n_long,
-            int long_th) {
+            int long_th, int l2pol) {
     const int64_t C = CC > 0 ? (int64_t)CC : C_rt;
-    const uint64_t pol_s = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();
+    const uint64_t pol_s = make_policy(l2pol & 0xf);
+    const uint64_t pol_x = make_policy(l2pol >> 4);
     const int64_t n_long_blocks = LONG ? (n_long + (kThreads / 32) - 1) / (kThreads / 32) : 0;
     if (LONG && (int64_t)blockIdx.x < n_long_blocks) {
         const int64_t k = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
@@ -325,14 +335,25 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     const int64_t n_long = m->long_rows ? m->n_long : 0;
     const int64_t long_blocks = (n_long + kThreads / 32 - 1) / (kThreads / 32);
     const unsigned grid = (unsigned)(grid_for(rows, kThreads) + long_blocks);
+    // L2 policies: matrix streams (low nibble) and x gathers (high nibble);
+    // 0 evict_first, 1 evict_normal, 2 evict_last.  x is always evict_last;
+    // the matrix stream is evict_first while x fits comfortably in L2 and
+    // evict_normal once it does not (measured: cfg2 987 vs 939
+    // GF/s, cfg5 612 vs 713 GF/s).  SELLB_L2POL overrides.
+    static const int l2pol_env = [] {
+        const char* e = getenv("SELLB_L2POL");
+        return e ? (int)strtol(e, nullptr, 0) : -1;
+    }();
+    const int l2pol = l2pol_env >= 0 ? l2pol_env
+                      : ((int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20);
     if (n_long)
         k_spmv_sell<T, CC, SKIP, ACC, ORD, 4, true><<<grid, kThreads, 0, st>>>(
             m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,
-            p0, p1, m->n_rows, m->long_rows, n_long, m->long_th);
+            p0, p1, m->n_rows, m->long_rows, n_long, m->long_th, l2pol);
     else
         k_spmv_sell<T, CC, SKIP, ACC, ORD, 4, false><<<grid, kThreads, 0, st>>>(
             m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,
-            p0, p1, m->n_rows, nullptr, 0, 0x7fffffff);
+            p0, p1, m->n_rows, nullptr, 0, 0x7fffffff, l2pol);
     return 0;
 }
 
