@@ -71,6 +71,10 @@ def make_matrix(config, rank=0, world=1):
         return None, f"3D 27-point stencil 128x128x{128 * world} (z-slabs)"
     if config == "cfg3":
         return generate.powerlaw(4_000_000), "power-law rows N=4M mean~20"
+    if config == "cfg4":
+        from paper_1307_6209_b200 import coo_to_crs, gen_skewed
+        return (coo_to_crs(gen_skewed(1 << 21, 8, 2048, 1024)),
+                "skewed N=2^21 base 8, 1024 spikes of 2048 (sellkit gen_skewed)")
     raise SystemExit(f"unknown config {config}")
 
 
@@ -193,14 +197,22 @@ def run_reference(args):
         return 0
     import oracle
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    sigma = args.sigma
     if args.config == "cfg2" and world > 1:
         from paper_1307_6209_b200 import generate
         crs = generate.stencil27(128, nz=128 * world)
         desc = f"3D 27-point stencil 128x128x{128 * world} (z-slabs)"
+    elif args.config == "cfg5":
+        # the host cannot hold 1.3e9 nonzeros through the reference's path:
+        # a 2^20-row block of the row-addressable matrix
+        from paper_1307_6209_b200 import CRSMatrix, generate
+        n = args.n or (1 << 26)
+        rp, cl_, vl = generate.hamiltonian_rows(n, 0, 1 << 20)
+        crs = CRSMatrix(1 << 20, n, rp, cl_, vl)
+        desc = f"rows [0, 2^20) of the banded-random N={n} matrix"
     else:
         crs, desc = make_matrix(args.config)
-    sigma = args.sigma
-    o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, 32, sigma)
+    o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, args.C, sigma)
     x = np.random.default_rng(12345).uniform(-1, 1, crs.n_cols)
     threads = os.cpu_count() or 1
     # size each step so warmup + steps finish within ~2 minutes
@@ -235,7 +247,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{desc}, SELL-32-{sigma}", "C": 32, "sigma": sigma,
+        "config": {"workload": f"{desc}, SELL-{args.C}-{sigma}", "C": args.C, "sigma": sigma,
                    "n_rows": crs.n_rows, "nnz": crs.nnz},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": len(spans),
                          "kind": "reference" if ref is not None else "port",
@@ -273,13 +285,13 @@ def host_workload(args, dt_np):
     x = np.random.default_rng(12345).uniform(-1, 1, crs.n_cols).astype(dt_np)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    s = sb.crs_to_sell(crs, 32, args.sigma, dtype=dt_np)
+    s = sb.crs_to_sell(crs, args.C, args.sigma, dtype=dt_np)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
 
     def parity(yd):
         o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val.astype(dt_np), crs.n_rows,
-                               crs.n_cols, 32, args.sigma)
+                               crs.n_cols, args.C, args.sigma)
         y_ref = oracle.spmv_sell(o, x, threads=os.cpu_count() or 1)
         ok = yd.cpu().numpy().tobytes() == y_ref.tobytes()
         return ok and all(getattr(s, k).tobytes() == getattr(o, k).tobytes() for k in ARRAYS)
@@ -310,7 +322,7 @@ def cfg5_workload(args, dt_np):
     t0 = time.perf_counter()
     rpt, col, val = generate.hamiltonian_device(n, device=0, dtype=dt_np)
     t_gen = time.perf_counter() - t0
-    s = sb.crs_to_sell_device(rpt, col, val, n, n, 32, sigma)
+    s = sb.crs_to_sell_device(rpt, col, val, n, n, args.C, sigma)
     del rpt, col, val
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -326,7 +338,7 @@ def cfg5_workload(args, dt_np):
         ok = True
         for r0 in (0, (n // 2) // blk * blk, n - blk):
             b = block(r0, r0 + blk)
-            o = oracle.crs_to_sell(b.rpt, b.col, b.val, b.n_rows, n, 32, sigma)
+            o = oracle.crs_to_sell(b.rpt, b.col, b.val, b.n_rows, n, args.C, sigma)
             got = s.export_range(r0 // 32, (r0 + blk) // 32)
             for k in ("cs", "cl", "col", "val", "row_lengths"):
                 ok = ok and got[k].tobytes() == getattr(o, k).tobytes()
@@ -336,7 +348,7 @@ def cfg5_workload(args, dt_np):
 
     def cpu(budget):
         b = block(0, min(n, 1 << 20))
-        o = oracle.crs_to_sell(b.rpt, b.col, b.val.astype(np.float64), b.n_rows, n, 32, sigma)
+        o = oracle.crs_to_sell(b.rpt, b.col, b.val.astype(np.float64), b.n_rows, n, args.C, sigma)
         gf, kind, cores, sample, _ = cpu_reference_run(o, x.astype(np.float64),
                                                        budget_s=budget)
         return {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": kind,
@@ -463,7 +475,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_ms, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": f"{desc}, SELL-32-{sigma}", "C": 32, "sigma": sigma,
+        "config": {"workload": f"{desc}, SELL-{args.C}-{sigma}", "C": args.C, "sigma": sigma,
                    "n_rows": n_rows, "nnz": nnz, "slots": slots,
                    "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
                    "l2": ("flushed between steps (%d MB scratch write); value from the "
@@ -495,13 +507,17 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--sigma", type=int, default=1)
+    ap.add_argument("--sigma", type=int, default=None,
+                    help="sorting scope (default 1; 512 for cfg5)")
+    ap.add_argument("--C", type=int, default=32, help="chunk height")
     ap.add_argument("--dtype", choices=("f64", "f32"), default="f64")
     ap.add_argument("--skip-parity", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--n", type=int, default=0, help="cfg5 rows (default 2^26)")
     args = ap.parse_args(argv)
+    if args.sigma is None:
+        args.sigma = 512 if args.config == "cfg5" else 1
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
