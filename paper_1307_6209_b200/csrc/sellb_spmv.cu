@@ -174,7 +174,7 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
 // long_th, rows longer than long_th belong to the long-row role and the
 // others stop at their own length (pad-skip semantics).
 template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U, bool LONG>
-__global__ void __launch_bounds__(kThreads, 8)
+__global__ void __launch_bounds__(kThreads, U == 4 ? 8 : 5)
 k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
@@ -346,14 +346,23 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     }();
     const int l2pol = l2pol_env >= 0 ? l2pol_env
                       : ((int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20);
-    if (n_long)
-        k_spmv_sell<T, CC, SKIP, ACC, ORD, 4, true><<<grid, kThreads, 0, st>>>(
-            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,
-            p0, p1, m->n_rows, m->long_rows, n_long, m->long_th, l2pol);
-    else
-        k_spmv_sell<T, CC, SKIP, ACC, ORD, 4, false><<<grid, kThreads, 0, st>>>(
-            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,
-            p0, p1, m->n_rows, nullptr, 0, 0x7fffffff, l2pol);
+    static const int u_env = [] {
+        const char* e = getenv("SELLB_U");
+        return e ? atoi(e) : 0;
+    }();
+    const bool u8 = u_env == 8;
+#define SELLB_LAUNCH(UU, LL, LR, NL, TH)                                                        \
+    k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(                      \
+        m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0, \
+        p1, m->n_rows, LR, NL, TH, l2pol)
+    if (n_long) {
+        if (u8) SELLB_LAUNCH(8, true, m->long_rows, n_long, m->long_th);
+        else SELLB_LAUNCH(4, true, m->long_rows, n_long, m->long_th);
+    } else {
+        if (u8) SELLB_LAUNCH(8, false, nullptr, 0, 0x7fffffff);
+        else SELLB_LAUNCH(4, false, nullptr, 0, 0x7fffffff);
+    }
+#undef SELLB_LAUNCH
     return 0;
 }
 
