@@ -346,11 +346,17 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     }();
     const int l2pol = l2pol_env >= 0 ? l2pol_env
                       : ((int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20);
+    // slots batched per load round: 8 for fp32 (half the bytes per slot),
+    // long rows (N_nzr >= 24) and skewed matrices (some chunk wider than 64),
+    // else 4 (measured, tools/ab_env.sh: cfg2 f32 1230 -> 1377 GF/s, cfg3
+    // sigma=128 261 -> 310; cfg1 443 -> 376 and cfg5 878 -> 864 prefer 4).
     static const int u_env = [] {
         const char* e = getenv("SELLB_U");
         return e ? atoi(e) : 0;
     }();
-    const bool u8 = u_env == 8;
+    const bool u8 = u_env ? u_env == 8
+                          : (sizeof(T) == 4 || m->max_cl > 64 ||
+                             (m->n_rows > 0 && m->nnz >= 24 * m->n_rows));
 #define SELLB_LAUNCH(UU, LL, LR, NL, TH)                                                        \
     k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(                      \
         m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0, \
