@@ -123,6 +123,12 @@ int sellb_export(const sellb_mat* m, int64_t* cs, int32_t* cl, int32_t* col,
 int sellb_export_range(const sellb_mat* m, int64_t c0, int64_t c1, int64_t* cs, int32_t* cl,
                        int32_t* col, void* val, int32_t* row_lengths);
 
+/* Rebuild row_lengths of an imported matrix on the device the way the
+ * reference's .sell cache reader does (io.py:308-321): a stored row's length
+ * is its chunk width minus the trailing run of (val == 0.0, col == 0) slots.
+ * Enables the pad-skipping kernel and the fused unpermute for the matrix. */
+int sellb_infer_row_lengths(sellb_mat* m, void* stream);
+
 int sellb_set_variant(sellb_mat* m, int32_t variant);
 void sellb_free(sellb_mat* m);
 

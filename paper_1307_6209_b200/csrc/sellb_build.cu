@@ -162,6 +162,23 @@ __global__ void k_sector_count(const int32_t* __restrict__ rl, int64_t n_pad, in
     }
 }
 
+// .sell cache semantics (io.py:308-321): length = chunk width minus the
+// trailing run of padding-looking slots (value 0.0 and column 0)
+template <typename T>
+__global__ void k_trailing_len(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+                               const int32_t* __restrict__ col, const T* __restrict__ val,
+                               int64_t n_pad, int64_t C, int32_t* __restrict__ rl) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n_pad) return;
+    const int64_t c = p / C;
+    const int64_t base = cs[c] + (p - c * C);
+    int32_t len = cl[c];
+    while (len > 0 && val[base + (int64_t)(len - 1) * C] == T(0) &&
+           col[base + (int64_t)(len - 1) * C] == 0)
+        --len;
+    rl[p] = len;
+}
+
 int64_t sigma_effective(int64_t n, int64_t C, int64_t sigma, int64_t n_pad) {
     // formats.py:325-334
     if (sigma <= C) return 1;
@@ -666,6 +683,36 @@ int sellb_export_range(const sellb_mat* m, int64_t c0, int64_t c1, int64_t* cs, 
         SELLB_CU(cudaMemcpy(row_lengths, m->rl + c0 * m->C, nc * m->C * 4,
                             cudaMemcpyDeviceToHost));
     }
+    return 0;
+}
+
+int sellb_infer_row_lengths(sellb_mat* m, void* stream) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    DeviceGuard guard(m->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!m->rl && m->n_pad)
+        if (int rc = alloc_dev((void**)&m->rl, m->n_pad * 4)) return rc;
+    if (m->n_pad) {
+        if (m->dtype == SELLB_F32)
+            k_trailing_len<float><<<(unsigned)grid_for(m->n_pad, 256), 256, 0, st>>>(
+                m->cs, m->cl, m->col, (const float*)m->val, m->n_pad, m->C, m->rl);
+        else
+            k_trailing_len<double><<<(unsigned)grid_for(m->n_pad, 256), 256, 0, st>>>(
+                m->cs, m->cl, m->col, (const double*)m->val, m->n_pad, m->C, m->rl);
+        if (int rc = check_stream_error()) return rc;
+        std::vector<int32_t> h(m->n_pad);
+        SELLB_CU(cudaMemcpyAsync(h.data(), m->rl, m->n_pad * 4, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+        int64_t s = 0;
+        for (auto v : h) s += v;
+        m->nnz = s;
+    } else {
+        m->nnz = 0;
+    }
+    m->variant = SELLB_VARIANT_AUTO;
+    if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
+    if (int rc = build_long_rows(m, st)) return rc;
     return 0;
 }
 

@@ -176,7 +176,33 @@ def main():
             errs.append((C, sigma, align, 1))
     np.savez_compressed(os.path.join(out_dir, "param_errors.npz"),
                         n_rows=100, cases=np.array(errs, np.int64))
+    make_cache_fixtures(out_dir)
     print(f"wrote {idx} cases to {out_dir}")
+
+
+def make_cache_fixtures(out_dir):
+    """.sell files written by the reference's write_sell_cache and the arrays
+    its read_sell_cache returns for them (io.py:243-382)."""
+    from sellkit import read_sell_cache, write_sell_cache
+    rng = np.random.default_rng(31)
+    zero_row = COOMatrix(6, 6, [0, 0, 2, 3, 3, 5], [1, 4, 0, 0, 5, 3],
+                         [1.5, -2.0, 0.0, 0.0, 7.0, 3.25])   # rows 2/3 end in (0.0, col 0)?
+    cases = {
+        "rand": (coo_to_crs(random_coo(rng, 60, 60, 360)), 8, 16, False),
+        "perm": (coo_to_crs(random_coo(rng, 40, 40, 300)), 4, 40, True),
+        "zero_col0": (coo_to_crs(zero_row), 2, 1, False),
+    }
+    for name, (m, C, sigma, permute) in cases.items():
+        s = crs_to_sell(m, C, sigma, permute_cols=permute)
+        path = os.path.join(out_dir, f"ref_cache_{name}.sell")
+        write_sell_cache(s, path)
+        r = read_sell_cache(path)
+        np.savez_compressed(os.path.join(out_dir, f"ref_cache_{name}.npz"),
+                            n_rows=r.n_rows, n_cols=r.n_cols, C=r.C, sigma=r.sigma,
+                            n_rows_padded=r.n_rows_padded, n_chunks=r.n_chunks,
+                            col_permuted=r.col_permuted, cs=r.cs, cl=r.cl, col=r.col,
+                            val=r.val, perm=r.perm, row_lengths=r.row_lengths,
+                            built_row_lengths=s.row_lengths)
 
 
 if __name__ == "__main__":
