@@ -111,9 +111,14 @@ __device__ __forceinline__ void store_row(T* __restrict__ y, const int32_t* __re
 
 // Long-row role: one WARP per stored row longer than long_th, lanes over
 // slots (lane l loads slot j0+l; stride C).  The rounded products are formed
-// in parallel, then summed in slot order through warp shuffles -- the same
-// sequence of roundings as the reference's per-row loop, so the result is
-// bitwise identical.  kSeg segments (kSeg*32 slots) are loaded per batch.
+// in parallel and staged in shared memory, then every lane sums the staged
+// products in slot order (broadcast reads, no shuffles in the add chain) --
+// the same sequence of roundings as the reference's per-row loop, so the
+// result is bitwise identical.  Slots past the row length stage +0.0, and
+// adding +0.0 to a sum that started at +0.0 is an exact no-op (the sum can
+// never be -0.0), so the chain needs no predicate.  kSeg*32 slots per batch.
+constexpr int kSeg = 4;
+
 template <typename T, bool ACC, int ORD>
 __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
                                          const int32_t* __restrict__ cl,
@@ -122,8 +127,7 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
                                          const T* __restrict__ val, const T* __restrict__ x,
                                          T* __restrict__ y, const int32_t* __restrict__ order,
                                          int64_t C, int64_t p, int64_t n_rows, int lane,
-                                         uint64_t pol_s, uint64_t pol_x) {
-    constexpr int kSeg = 4;
+                                         uint64_t pol_s, uint64_t pol_x, T* __restrict__ stage) {
     const int64_t chunk = p / C;
     const int64_t base = cs[chunk] + (p - chunk * C);
     const int w = cl[chunk];
@@ -150,16 +154,20 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
             const int j = j0 + s * 32 + lane;
             prod[s] = (j < len) ? Arith<T>::mul(v[s], ld_x(x + c[s], pol_x)) : T(0);
         }
+        __syncwarp();                        // previous batch fully consumed
 #pragma unroll
-        for (int s = 0; s < kSeg; ++s) {
-            const int rem = len - (j0 + s * 32);          // warp-uniform
-            const int n = rem < 32 ? rem : 32;
-#pragma unroll 8
-            for (int i = 0; i < 32; ++i) {
-                const T q = __shfl_sync(0xffffffffu, prod[s], i);
-                if (i < n) sum = Arith<T>::add(sum, q);
-            }
+        for (int s = 0; s < kSeg; ++s) stage[s * 32 + lane] = prod[s];
+        __syncwarp();
+        const int nb = min(len - j0, kSeg * 32);      // warp-uniform
+        int i = 0;
+        for (; i + 16 <= nb; i += 16) {
+            T q[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) q[k] = stage[i + k];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) sum = Arith<T>::add(sum, q[k]);
         }
+        for (; i < nb; ++i) sum = Arith<T>::add(sum, stage[i]);
     }
     if (len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
     if (lane == 0) store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
@@ -174,7 +182,7 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
 // long_th, rows longer than long_th belong to the long-row role and the
 // others stop at their own length (pad-skip semantics).
 template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U, bool LONG>
-__global__ void __launch_bounds__(kThreads, U == 4 ? 8 : 5)
+__global__ void __launch_bounds__(kThreads, U == 4 ? (LONG ? 6 : 8) : 5)
 k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
@@ -185,14 +193,17 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     const uint64_t pol_s = make_policy(l2pol & 0xf);
     const uint64_t pol_x = make_policy(l2pol >> 4);
     const int64_t n_long_blocks = LONG ? (n_long + (kThreads / 32) - 1) / (kThreads / 32) : 0;
-    if (LONG && (int64_t)blockIdx.x < n_long_blocks) {
-        const int64_t k = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-        if (k >= n_long) return;
-        const int64_t p = long_rows[k];
-        if (p < p0 || p >= p1) return;
-        long_row<T, ACC, ORD>(cs, cl, rl, col, val, x, y, order, C, p, n_rows,
-                              threadIdx.x & 31, pol_s, pol_x);
-        return;
+    if constexpr (LONG) {
+        if ((int64_t)blockIdx.x < n_long_blocks) {
+            __shared__ T stage[kThreads / 32][kSeg * 32];
+            const int64_t k = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+            if (k >= n_long) return;
+            const int64_t p = long_rows[k];
+            if (p < p0 || p >= p1) return;
+            long_row<T, ACC, ORD>(cs, cl, rl, col, val, x, y, order, C, p, n_rows,
+                                  threadIdx.x & 31, pol_s, pol_x, stage[threadIdx.x >> 5]);
+            return;
+        }
     }
     const int64_t p = p0 + ((int64_t)blockIdx.x - n_long_blocks) * kThreads + threadIdx.x;
     if (p >= p1) return;
