@@ -204,6 +204,7 @@ void free_mat_arrays(sellb_mat* m) {
     cudaFree(m->perm);
     cudaFree(m->order);
     cudaFree(m->long_rows);
+    cudaFree(m->chunk_th);
     if (m->pipe_ready) {
         cudaStreamDestroy(m->s_h2d);
         cudaStreamDestroy(m->s_comp);
@@ -270,20 +271,42 @@ int choose_variant(sellb_mat* m, cudaStream_t st, double* beta_eff_out, int64_t*
 // Default threshold 256 slots (SELLB_LONG_TH overrides; <= 0 disables).
 int build_long_rows(sellb_mat* m, cudaStream_t st) {
     cudaFree(m->long_rows);
+    cudaFree(m->chunk_th);
     m->long_rows = nullptr;
+    m->chunk_th = nullptr;
     m->n_long = 0;
     m->long_th = 0x7fffffff;
     if (!m->rl || m->n_pad == 0) return 0;
-    int th = 256;
-    if (const char* e = getenv("SELLB_LONG_TH")) th = atoi(e);
+    // Two thresholds: a row longer than th_lo leaves the bulk role when its
+    // chunk is heterogeneous (shortest row < 1/4 of the widest: the warp
+    // would run mostly idle lanes), and any row longer than th_hi leaves it
+    // (one thread's latency chain).  Sorted chunks of similar long rows stay
+    // in the coalesced bulk role up to th_hi (measured: cfg3 sigma=N 693 ->
+    // 742 GF/s with the threshold raised from 256 to 512).
+    int th = 256, th_hi = 1024;
+    if (const char* e = getenv("SELLB_LONG_TH")) th = th_hi = atoi(e);
+    if (const char* e = getenv("SELLB_LONG_TH_HI")) th_hi = atoi(e);
     if (th <= 0 || m->max_cl <= th) return 0;
-    std::vector<int32_t> h_rl(m->n_pad);
+    std::vector<int32_t> h_rl(m->n_pad), h_cl(m->n_chunks);
     SELLB_CU(cudaMemcpyAsync(h_rl.data(), m->rl, m->n_pad * 4, cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaMemcpyAsync(h_cl.data(), m->cl, m->n_chunks * 4, cudaMemcpyDeviceToHost, st));
     SELLB_CU(cudaStreamSynchronize(st));
-    std::vector<int32_t> rows;
-    for (int64_t p = 0; p < m->n_pad; ++p)
-        if (h_rl[p] > th) rows.push_back((int32_t)p);
+    std::vector<int32_t> cth(m->n_chunks, th_hi), rows;
+    for (int64_t c = 0; c < m->n_chunks; ++c) {
+        if (h_cl[c] <= th) continue;
+        int32_t lo = 0x7fffffff, hi = 0;
+        for (int64_t r = 0; r < m->C; ++r) {
+            lo = std::min(lo, h_rl[c * m->C + r]);
+            hi = std::max(hi, h_rl[c * m->C + r]);
+        }
+        if ((int64_t)lo * 4 < hi) cth[c] = th;
+        for (int64_t r = 0; r < m->C; ++r)
+            if (h_rl[c * m->C + r] > cth[c]) rows.push_back((int32_t)(c * m->C + r));
+    }
     if (rows.empty()) return 0;
+    if (int rc = alloc_dev((void**)&m->chunk_th, m->n_chunks * 4)) return rc;
+    SELLB_CU(cudaMemcpyAsync(m->chunk_th, cth.data(), m->n_chunks * 4, cudaMemcpyHostToDevice,
+                             st));
     std::stable_sort(rows.begin(), rows.end(),
                      [&](int32_t a, int32_t b) { return h_rl[a] > h_rl[b]; });
     if (int rc = alloc_dev((void**)&m->long_rows, rows.size() * 4)) return rc;

@@ -42,7 +42,8 @@ struct sellb_mat {
     // warp-per-row role (lanes over slots) takes them
     int32_t* long_rows = nullptr;
     int64_t n_long = 0;
-    int32_t long_th = 0x7fffffff;
+    int32_t long_th = 0x7fffffff;     // chunks wider than this may hold long rows
+    int32_t* chunk_th = nullptr;      // per chunk: rows longer than this are long
     // end-to-end staging (device x / y for sellb_spmv_host)
     void* x_buf = nullptr;
     void* y_buf = nullptr;

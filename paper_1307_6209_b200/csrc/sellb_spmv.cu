@@ -179,7 +179,8 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
 // in [p0, p1) (the paper's GPU design; for C = 32 a warp owns a chunk).
 // CC > 0: compile-time chunk height.  ORD 0: y[p] in stored order; ORD 1:
 // y[order[p]] for real rows (fused unpermute).  In chunks wider than
-// long_th, rows longer than long_th belong to the long-row role and the
+// long_th, rows longer than the chunk's threshold chunk_th[] belong to the
+// long-row role (the same rule builds long_rows[], sellb_build.cu) and the
 // others stop at their own length (pad-skip semantics).
 template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U, bool LONG>
 __global__ void __launch_bounds__(kThreads, U == 4 ? (LONG ? 6 : 8) : 5)
@@ -188,7 +189,7 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
             const int32_t* __restrict__ order, int64_t C_rt, int64_t p0, int64_t p1,
             int64_t n_rows, const int32_t* __restrict__ long_rows, int64_t n_long,
-            int long_th, int l2pol) {
+            int long_th, const int32_t* __restrict__ chunk_th, int l2pol) {
     const int64_t C = CC > 0 ? (int64_t)CC : C_rt;
     const uint64_t pol_s = make_policy(l2pol & 0xf);
     const uint64_t pol_x = make_policy(l2pol >> 4);
@@ -212,9 +213,9 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     const int w = cl[chunk];
     int len = SKIP ? rl[p] : w;
     bool skip_pad = SKIP;
-    if (LONG && w > long_th) {           // a chunk holding long rows
+    if (LONG && w > long_th) {           // a chunk that may hold long rows
         if (!SKIP) len = rl[p];
-        if (len > long_th) return;       // owned by the long-row role
+        if (len > chunk_th[chunk]) return;   // owned by the long-row role
         skip_pad = true;
     }
     const T* vp = val + base;
@@ -371,7 +372,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
 #define SELLB_LAUNCH(UU, LL, LR, NL, TH)                                                        \
     k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(                      \
         m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0, \
-        p1, m->n_rows, LR, NL, TH, l2pol)
+        p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol)
     if (n_long) {
         if (u8) SELLB_LAUNCH(8, true, m->long_rows, n_long, m->long_th);
         else SELLB_LAUNCH(4, true, m->long_rows, n_long, m->long_th);
