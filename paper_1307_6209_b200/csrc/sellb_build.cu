@@ -283,7 +283,7 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     // (one thread's latency chain).  Sorted chunks of similar long rows stay
     // in the coalesced bulk role up to th_hi (measured: cfg3 sigma=N 693 ->
     // 742 GF/s with the threshold raised from 256 to 512).
-    int th = 256, th_hi = 1024;
+    int th = 256, th_hi = 512;      // th_hi 512/1024/2048 on cfg3 sigma=N: 742/674/426
     if (const char* e = getenv("SELLB_LONG_TH")) th = th_hi = atoi(e);
     if (const char* e = getenv("SELLB_LONG_TH_HI")) th_hi = atoi(e);
     if (th <= 0 || m->max_cl <= th) return 0;
