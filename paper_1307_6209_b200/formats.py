@@ -282,8 +282,11 @@ class SellMatrix:
     def handle(self):
         """The ``sellb_mat*`` (uploads host-constructed matrices on first use)."""
         if self._handle is None:
-            lib = _lib.require_device()
             h = self._host
+            if any(h.get(k) is None for k in _ARRAYS):
+                from .errors import ResourceError
+                raise ResourceError("the matrix's device copy was freed")
+            lib = _lib.require_device()
             out = ctypes.c_void_p()
             dt = _lib.SELLB_F32 if self.dtype == np.float32 else _lib.SELLB_F64
             _lib.check(lib.sellb_import(
@@ -305,6 +308,16 @@ class SellMatrix:
         d = _lib.DevArrays()
         _lib.check(_lib.load().sellb_device_arrays(self.handle, ctypes.byref(d)))
         return {name: getattr(d, name) for name, _ in d._fields_}
+
+    def sector_occupancy(self):
+        """(beta_eff, val_sectors, col_sectors): occupancy counted in the
+        32-byte sectors the pad-skipping kernel touches."""
+        be = ctypes.c_double()
+        vs, cs = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.load().sellb_sector_occupancy(self.handle, ctypes.byref(be),
+                                                      ctypes.byref(vs), ctypes.byref(cs),
+                                                      None))
+        return float(be.value), int(vs.value), int(cs.value)
 
     def export_range(self, c0, c1):
         """Host copies of chunks [c0, c1): cs (rebased), cl, col, val and
@@ -336,9 +349,9 @@ class SellMatrix:
         _lib.check(_lib.load().sellb_set_variant(self.handle, code))
 
     def free(self):
-        """Release the device copy now (host arrays stay if exported)."""
+        """Release the device copy now (host arrays already exported stay;
+        nothing is exported on the way out)."""
         if self._finalizer is not None:
-            self._export_all()
             self._finalizer()
             self._finalizer = None
             self._handle = None

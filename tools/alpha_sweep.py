@@ -1,0 +1,130 @@
+#!/usr/bin/env python3
+"""sigma sweep with the performance model fed by MEASURED DRAM bytes -- the
+B200 analog of the reference's `sellkit sweep-sigma` (cli.py:296-320), which
+simulates alpha with an LRU model (cachesim.py:49-75).  Here alpha comes from
+ncu's dram__bytes_read.sum + dram__bytes_write.sum of the SpMV kernel.
+
+On the GPU box (one ncu pass, one SpMV launch per layout):
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+        -k regex:k_spmv_sell --csv --log-file gpurun_out/alpha.csv \
+        python tools/alpha_sweep.py run gpurun_out/alpha_layouts.json
+and without ncu for timing:
+    python tools/alpha_sweep.py time gpurun_out/alpha_times.json
+Here (CPU):
+    python tools/alpha_sweep.py report gpurun_out/alpha_layouts.json \
+        gpurun_out/alpha.csv gpurun_out/alpha_times.json > profiles/r01_alpha_sweep.md
+"""
+import csv
+import io
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+LAYOUTS = [("cfg2", 1)] + [("cfg3", s) for s in (1, 32, 64, 128, 256, 512, 1024, 4096,
+                                                  4_000_000)]
+
+
+def matrices():
+    from paper_1307_6209_b200 import generate
+    cache = {}
+    for name, sigma in LAYOUTS:
+        if name not in cache:
+            cache[name] = generate.stencil27(128) if name == "cfg2" else generate.powerlaw()
+        yield name, sigma, cache[name]
+
+
+def run(out_json, timed=False):
+    import numpy as np
+    import torch
+    import paper_1307_6209_b200 as sb
+    from paper_1307_6209_b200 import generate
+    rows = []
+    for name, sigma, m in matrices():
+        s = sb.crs_to_sell(m, 32, sigma)
+        info = s.info()
+        be, vs, cs = s.sector_occupancy()
+        x = torch.from_numpy(generate.rhs(m.n_cols)).cuda()
+        y = torch.zeros(s.n_rows_padded, dtype=torch.float64, device="cuda")
+        rec = {"name": name, "sigma": sigma, "nnz": info.nnz, "n_rows": info.n_rows,
+               "n_cols": info.n_cols, "n_pad": info.n_rows_padded, "n_chunks": info.n_chunks,
+               "slots": info.slots, "beta": info.nnz / info.slots, "beta_eff": be,
+               "val_sectors": vs, "col_sectors": cs, "variant": s.variant}
+        if timed:
+            for _ in range(5):
+                sb.spmv_sell(s, x, y)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(50):
+                sb.spmv_sell(s, x, y)
+            e1.record()
+            e1.synchronize()
+            rec["kernel_s"] = e0.elapsed_time(e1) / 50 / 1e3
+        else:
+            sb.spmv_sell(s, x, y)            # the one profiled launch
+            torch.cuda.synchronize()
+        rows.append(rec)
+        s.free()
+    json.dump(rows, open(out_json, "w"), indent=1)
+
+
+def report(layouts_json, ncu_csv, times_json):
+    from paper_1307_6209_b200 import model
+    rows = json.load(open(layouts_json))
+    times = {(r["name"], r["sigma"]): r["kernel_s"] for r in json.load(open(times_json))}
+    lines = open(ncu_csv).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    recs = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+    per = {}
+    for r in recs:
+        per.setdefault(r["ID"], {})[r["Metric Name"]] = (float(r["Metric Value"]),
+                                                         r["Metric Unit"])
+    ids = sorted(per, key=int)
+    assert len(ids) == len(rows), (len(ids), len(rows))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
+    print("# sigma sweep with measured alpha (one B200)\n")
+    print("alpha_paper = `infer_alpha(dram, nnz, beta, N_nzr, line=32)` (model.py:124-142 "
+          "with B200's 32 B sector as the line); alpha_eff = `alpha_from_traffic` with the "
+          "bytes the kernel variant actually streams (all slots for pad-incl, touched sectors "
+          "+ row_lengths for pad-skip).  Ideal alpha = 1/N_nzc.  DRAM = ncu "
+          "dram__bytes_read.sum + dram__bytes_write.sum of one cold SpMV launch; "
+          "GF/s from CUDA events (50 warm launches).\n")
+    print("| matrix | sigma | beta | beta_eff | variant | DRAM MB | V_alg MB | alpha_paper | "
+          "in range | alpha_eff | ideal alpha | B paper (ideal alpha) | GF/s | paper P = b/B GF/s |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+    for i, row in zip(ids, rows):
+        d = per[i]
+        rd = d["dram__bytes_read.sum"][0] * scale[d["dram__bytes_read.sum"][1]]
+        wr = d["dram__bytes_write.sum"][0] * scale[d["dram__bytes_write.sum"][1]]
+        dram = rd + wr
+        nnz, n = row["nnz"], row["n_rows"]
+        nzr, nzc = nnz / n, nnz / row["n_cols"]
+        a_p = model.infer_alpha(dram, nnz, row["beta"], nzr, line_bytes=32)
+        if row["variant"] == "pad_incl":
+            mat = 12 * row["slots"]
+            extra = 0
+        else:
+            mat = 32 * (row["val_sectors"] + row["col_sectors"])
+            extra = 4 * row["n_pad"]
+        a_e = model.alpha_from_traffic(dram, nnz, mat, row["n_pad"], row["n_chunks"],
+                                       extra_bytes=extra)
+        v_alg = model.algorithmic_bytes(nnz, row["n_cols"], row["n_pad"], row["n_chunks"])
+        bal = model.code_balance_sell(1.0 / nzc, row["beta"], nzr)
+        t = times[(row["name"], row["sigma"])]
+        print(f"| {row['name']} | {row['sigma']} | {row['beta']:.4f} | {row['beta_eff']:.4f} | "
+              f"{row['variant']} | {dram / 1e6:.1f} | {v_alg / 1e6:.1f} | {a_p.alpha:.3f} | "
+              f"{a_p.in_range} | {a_e.alpha:.3f} | {1 / nzc:.3f} | {bal:.3f} | "
+              f"{2 * nnz / t / 1e9:.1f} | {peak / bal:.1f} |")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "run":
+        run(sys.argv[2])
+    elif sys.argv[1] == "time":
+        run(sys.argv[2], timed=True)
+    else:
+        report(sys.argv[2], sys.argv[3], sys.argv[4])
