@@ -47,10 +47,15 @@ def run(out_json, timed=False):
         be, vs, cs = s.sector_occupancy()
         x = torch.from_numpy(generate.rhs(m.n_cols)).cuda()
         y = torch.zeros(s.n_rows_padded, dtype=torch.float64, device="cuda")
+        rl = s.row_lengths
+        # 64-byte granularity (two sectors): 8 fp64 lanes of val, 16 of col
+        v64 = int(rl.reshape(-1, 8).max(1).sum()) * 2
+        c64 = int(rl.reshape(-1, 16).max(1).sum()) * 2
         rec = {"name": name, "sigma": sigma, "nnz": info.nnz, "n_rows": info.n_rows,
                "n_cols": info.n_cols, "n_pad": info.n_rows_padded, "n_chunks": info.n_chunks,
                "slots": info.slots, "beta": info.nnz / info.slots, "beta_eff": be,
-               "val_sectors": vs, "col_sectors": cs, "variant": s.variant}
+               "val_sectors": vs, "col_sectors": cs, "val_sectors64": v64,
+               "col_sectors64": c64, "variant": s.variant}
         if timed:
             for _ in range(5):
                 sb.spmv_sell(s, x, y)
@@ -93,9 +98,10 @@ def report(layouts_json, ncu_csv, times_json):
           "+ row_lengths for pad-skip).  Ideal alpha = 1/N_nzc.  DRAM = ncu "
           "dram__bytes_read.sum + dram__bytes_write.sum of one cold SpMV launch; "
           "GF/s from CUDA events (50 warm launches).\n")
-    print("| matrix | sigma | beta | beta_eff | variant | DRAM MB | V_alg MB | alpha_paper | "
-          "in range | alpha_eff | ideal alpha | B paper (ideal alpha) | GF/s | paper P = b/B GF/s |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+    print("| matrix | sigma | beta | beta_eff | variant | DRAM MB | V_alg MB | matrix MB (32 B / 64 B) | "
+          "alpha_paper | in range | alpha_eff 32 B | alpha_eff 64 B | ideal alpha | "
+          "B paper (ideal alpha) | GF/s | paper P = b/B GF/s |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for i, row in zip(ids, rows):
         d = per[i]
         rd = d["dram__bytes_read.sum"][0] * scale[d["dram__bytes_read.sum"][1]]
@@ -105,19 +111,23 @@ def report(layouts_json, ncu_csv, times_json):
         nzr, nzc = nnz / n, nnz / row["n_cols"]
         a_p = model.infer_alpha(dram, nnz, row["beta"], nzr, line_bytes=32)
         if row["variant"] == "pad_incl":
-            mat = 12 * row["slots"]
+            mat = mat64 = 12 * row["slots"]
             extra = 0
         else:
             mat = 32 * (row["val_sectors"] + row["col_sectors"])
+            mat64 = 32 * (row["val_sectors64"] + row["col_sectors64"])
             extra = 4 * row["n_pad"]
         a_e = model.alpha_from_traffic(dram, nnz, mat, row["n_pad"], row["n_chunks"],
                                        extra_bytes=extra)
+        a_64 = model.alpha_from_traffic(dram, nnz, mat64, row["n_pad"], row["n_chunks"],
+                                        extra_bytes=extra)
         v_alg = model.algorithmic_bytes(nnz, row["n_cols"], row["n_pad"], row["n_chunks"])
         bal = model.code_balance_sell(1.0 / nzc, row["beta"], nzr)
         t = times[(row["name"], row["sigma"])]
         print(f"| {row['name']} | {row['sigma']} | {row['beta']:.4f} | {row['beta_eff']:.4f} | "
-              f"{row['variant']} | {dram / 1e6:.1f} | {v_alg / 1e6:.1f} | {a_p.alpha:.3f} | "
-              f"{a_p.in_range} | {a_e.alpha:.3f} | {1 / nzc:.3f} | {bal:.3f} | "
+              f"{row['variant']} | {dram / 1e6:.1f} | {v_alg / 1e6:.1f} | "
+              f"{mat / 1e6:.0f} / {mat64 / 1e6:.0f} | {a_p.alpha:.3f} | "
+              f"{a_p.in_range} | {a_e.alpha:.3f} | {a_64.alpha:.3f} | {1 / nzc:.3f} | {bal:.3f} | "
               f"{2 * nnz / t / 1e9:.1f} | {peak / bal:.1f} |")
 
 
