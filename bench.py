@@ -417,11 +417,17 @@ def run_ours(args):
         flush = torch.empty(4 * l2_bytes, dtype=torch.uint8, device=dev)
 
     # timed region: K steps, per-step events on the launching stream
+    # Without a flush every step is exactly one SpMV launch, back to back on
+    # one stream, so the region's two events give the average launch time
+    # (per-launch event pairs would add ~3 us of gap per launch).  With a
+    # flush, each SpMV gets its own event pair and the flushes are excluded.
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+          for _ in range(args.steps)] if flush is not None else []
     clocks = ClockSampler(0)
     clocks.start()
     time.sleep(0.25)
+    for _ in range(3):                 # re-warm after the idle sampler start
+        launch()
     torch.cuda.synchronize()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -429,15 +435,19 @@ def run_ours(args):
     for i in range(args.steps):
         if flush is not None:           # outside the kernel's event pair
             _lib.check(lib.sellb_l2_flush(flush.data_ptr(), flush.numel(), sp))
-        ev[i][0].record(stream)
-        launch()
-        ev[i][1].record(stream)
+            ev[i][0].record(stream)
+            launch()
+            ev[i][1].record(stream)
+        else:
+            launch()
     t_end.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     total_ms = t_start.elapsed_time(t_end)
-    per = [a.elapsed_time(b) for a, b in ev]
-    kern_ms = statistics.mean(per)
+    if flush is not None:
+        kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    else:
+        kern_ms = total_ms / args.steps
     # with an L2 flush between steps the step time is the SpMV's own events
     step_ms = kern_ms if flush is not None else total_ms / args.steps
     value = 2.0 * nnz / (step_ms / 1e3) / 1e9

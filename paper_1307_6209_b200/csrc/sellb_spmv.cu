@@ -183,7 +183,7 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
 // long-row role (the same rule builds long_rows[], sellb_build.cu) and the
 // others stop at their own length (pad-skip semantics).
 template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U, bool LONG>
-__global__ void __launch_bounds__(kThreads, U == 4 ? (LONG ? 6 : 8) : 5)
+__global__ void __launch_bounds__(kThreads, U == 4 ? (LONG ? 6 : 8) : (U == 6 ? 6 : 5))
 k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
@@ -376,6 +376,9 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     if (n_long) {
         if (u8) SELLB_LAUNCH(8, true, m->long_rows, n_long, m->long_th);
         else SELLB_LAUNCH(4, true, m->long_rows, n_long, m->long_th);
+    } else if (u_env == 6 || (!u_env && m->max_cl > 4 && m->max_cl <= 6 && sizeof(T) == 8)) {
+        // every chunk fits one 6-slot batch (5-point stencils): one round trip
+        SELLB_LAUNCH(6, false, nullptr, 0, 0x7fffffff);
     } else {
         if (u8) SELLB_LAUNCH(8, false, nullptr, 0, 0x7fffffff);
         else SELLB_LAUNCH(4, false, nullptr, 0, 0x7fffffff);
