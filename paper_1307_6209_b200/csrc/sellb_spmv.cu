@@ -598,23 +598,37 @@ int spmv_host_pipelined(sellb_mat* m, const void* x_host, void* y_host, cudaStre
                                      (b - a) * vs, cudaMemcpyHostToDevice, m->s_h2d));
         SELLB_CU(cudaEventRecord(m->ev_x[i], m->s_h2d));
     }
+    // Pinned (mapped) y: the kernels store y straight into host memory over
+    // PCIe (coalesced 256 B posted writes per warp), so the D2H direction
+    // needs no copy engine pass at all and overlaps the compute by
+    // construction.  Pageable y: per-block D2H copies on the second engine.
+    void* y_dev_view = nullptr;
+    {
+        cudaPointerAttributes at{};
+        if (!getenv("SELLB_NO_ZEROCOPY") &&
+            cudaPointerGetAttributes(&at, y_host) == cudaSuccess &&
+            at.type == cudaMemoryTypeHost && at.devicePointer)
+            y_dev_view = at.devicePointer;
+        cudaGetLastError();   // clear a "not registered" status for pageable memory
+    }
     int waited = -1;
     for (int b = 0; b < P; ++b) {
         if (m->blk_need[b] > waited) {
             SELLB_CU(cudaStreamWaitEvent(m->s_comp, m->ev_x[m->blk_need[b]], 0));
             waited = m->blk_need[b];
         }
-        if (int rc = launch_spmv(m, m->x_buf, m->y_buf, m->blk_c[b], m->blk_c[b + 1], 0,
-                                 SELLB_ORDER_STORED, m->s_comp))
+        if (int rc = launch_spmv(m, m->x_buf, y_dev_view ? y_dev_view : m->y_buf, m->blk_c[b],
+                                 m->blk_c[b + 1], 0, SELLB_ORDER_STORED, m->s_comp))
             return rc;
         SELLB_CU(cudaEventRecord(m->ev_blk[b], m->s_comp));
+        if (y_dev_view) continue;
         SELLB_CU(cudaStreamWaitEvent(m->s_d2h, m->ev_blk[b], 0));
         const int64_t y0 = m->blk_c[b] * m->C, y1 = m->blk_c[b + 1] * m->C;
         if (y1 > y0)
             SELLB_CU(cudaMemcpyAsync((char*)y_host + y0 * vs, (const char*)m->y_buf + y0 * vs,
                                      (y1 - y0) * vs, cudaMemcpyDeviceToHost, m->s_d2h));
     }
-    SELLB_CU(cudaStreamSynchronize(m->s_d2h));
+    SELLB_CU(cudaStreamSynchronize(y_dev_view ? m->s_comp : m->s_d2h));
     SELLB_CU(cudaStreamSynchronize(m->s_h2d));
     if (getenv("SELLB_PIPE_TRACE")) {        // debug timeline (events carry timing)
         float t;
