@@ -541,7 +541,7 @@ __global__ void k_chunk_maxcol(const int64_t* __restrict__ cs, const int32_t* __
 // landed).
 int pipe_setup(sellb_mat* m) {
     if (m->pipe_ready) return 0;
-    int want = 5;   // tools/e2e_probe.py on cfg2 picks the depth
+    int want = 4;   // tools/e2e_probe.py on cfg2: depth 2/4/8 -> 0.571/0.499-0.559/0.643 ms
     if (const char* e = getenv("SELLB_PIPE")) want = std::max(1, std::min(atoi(e), sellb_mat::kPipe));
     const int P = (int)std::min<int64_t>(want, std::max<int64_t>(m->n_chunks, 1));
     std::vector<int32_t> maxcol(std::max<int64_t>(m->n_chunks, 1), 0);
@@ -557,12 +557,13 @@ int pipe_setup(sellb_mat* m) {
     // x piece b ends just past the highest column row block b reads, so block
     // b can start as soon as piece b has landed (for banded matrices the
     // pieces then track the row blocks and H2D, compute and D2H overlap)
-    // Row blocks grow geometrically (1, 1, 2, 4, 8, ... parts): the first
-    // block's x lands early, and after that each block's y drain covers the
-    // next block's x transfer.  SELLB_PIPE_RAMP=0 gives equal blocks.
+    // Equal row blocks.  SELLB_PIPE_RAMP=1 makes them grow geometrically (1,
+    // 1, 2, 4, ... parts) -- measured slower on cfg2 (0.546 vs 0.499 ms):
+    // with both PCIe directions busy each runs at ~40 GB/s, and the y drain
+    // of a block is as long as the next block's x transfer anyway.
     m->n_pieces = P;
     m->x_off[0] = 0;
-    const bool ramp = !(getenv("SELLB_PIPE_RAMP") && atoi(getenv("SELLB_PIPE_RAMP")) == 0);
+    const bool ramp = getenv("SELLB_PIPE_RAMP") && atoi(getenv("SELLB_PIPE_RAMP")) == 1;
     std::vector<int64_t> wsum(P + 1, 0);
     for (int b = 0; b < P; ++b)
         wsum[b + 1] = wsum[b] + (ramp ? (b == 0 ? 1 : (1LL << (b - 1))) : 1);
