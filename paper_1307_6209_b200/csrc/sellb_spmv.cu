@@ -109,6 +109,53 @@ __device__ __forceinline__ void store_row(T* __restrict__ y, const int32_t* __re
     }
 }
 
+// One row's sum over its first len slots (stride C): U-slot batches -- all
+// val/col loads of the batch, then the U x gathers, then the adds in slot
+// order; a predicated tail batch finishes rows whose length is not a
+// multiple of U.
+template <typename T, int U>
+__device__ __forceinline__ T row_sum(const T* __restrict__ vp, const int32_t* __restrict__ cp,
+                                     int64_t C, int len, const T* __restrict__ x,
+                                     uint64_t pol_s, uint64_t pol_x) {
+    T sum = T(0);
+    int j = 0;
+    for (; j + U <= len; j += U) {
+        T v[U];
+        int32_t c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            v[u] = ld_stream(vp + (int64_t)(j + u) * C, pol_s);
+            c[u] = ld_stream(cp + (int64_t)(j + u) * C, pol_s);
+        }
+        T xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u], pol_x);
+#pragma unroll
+        for (int u = 0; u < U; ++u) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
+    }
+    if (j < len) {   // predicated tail batch
+        T v[U];
+        int32_t c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (j + u < len) {
+                v[u] = ld_stream(vp + (int64_t)(j + u) * C, pol_s);
+                c[u] = ld_stream(cp + (int64_t)(j + u) * C, pol_s);
+            } else {
+                v[u] = T(0);
+                c[u] = 0;
+            }
+        }
+        T xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = (j + u < len) ? ld_x(x + c[u], pol_x) : T(0);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (j + u < len) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
+    }
+    return sum;
+}
+
 // Long-row role: one WARP per stored row longer than long_th, lanes over
 // slots (lane l loads slot j0+l; stride C).  The rounded products are formed
 // in parallel and staged in shared memory, then every lane sums the staged
@@ -220,44 +267,50 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     }
     const T* vp = val + base;
     const int32_t* cp = col + base;
-    T sum = T(0);
-    int j = 0;
-    for (; j + U <= len; j += U) {
-        T v[U];
-        int32_t c[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            v[u] = ld_stream(vp + (int64_t)(j + u) * C, pol_s);
-            c[u] = ld_stream(cp + (int64_t)(j + u) * C, pol_s);
-        }
-        T xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u], pol_x);
-#pragma unroll
-        for (int u = 0; u < U; ++u) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
-    }
-    if (j < len) {   // predicated tail batch
-        T v[U];
-        int32_t c[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (j + u < len) {
-                v[u] = ld_stream(vp + (int64_t)(j + u) * C, pol_s);
-                c[u] = ld_stream(cp + (int64_t)(j + u) * C, pol_s);
-            } else {
-                v[u] = T(0);
-                c[u] = 0;
-            }
-        }
-        T xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = (j + u < len) ? ld_x(x + c[u], pol_x) : T(0);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (j + u < len) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
-    }
+    T sum = row_sum<T, U>(vp, cp, C, len, x, pol_s, pol_x);
     if (skip_pad && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
     store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
+}
+
+// Persistent "short chunk" variant (C = 32, no long rows): a grid of a few
+// blocks per SM whose warps sweep chunks c, c + n_warps, ...; the next
+// chunk's metadata (cs, cl, row length) is fetched before the current chunk
+// is multiplied, taking one dependent DRAM round trip off every chunk and
+// removing the partial last wave of a one-warp-per-chunk grid.
+template <typename T, bool SKIP, bool ACC, int ORD, int U>
+__global__ void __launch_bounds__(kThreads, 6)
+k_spmv_sell_sweep(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+                  const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+                  const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+                  const int32_t* __restrict__ order, int64_t c0, int64_t c1, int64_t n_rows,
+                  int l2pol) {
+    const uint64_t pol_s = make_policy(l2pol & 0xf);
+    const uint64_t pol_x = make_policy(l2pol >> 4);
+    const int lane = threadIdx.x & 31;
+    const int64_t n_warps = (int64_t)gridDim.x * (kThreads / 32);
+    int64_t c = c0 + (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    if (c >= c1) return;
+    int64_t base = cs[c];
+    int w = cl[c];
+    int len = SKIP ? rl[c * 32 + lane] : w;
+    while (true) {
+        const int64_t cn = c + n_warps;
+        int64_t base_n = 0;
+        int w_n = 0, len_n = 0;
+        if (cn < c1) {                       // prefetch the next chunk's metadata
+            base_n = cs[cn];
+            w_n = cl[cn];
+            len_n = SKIP ? rl[cn * 32 + lane] : 0;
+        }
+        T sum = row_sum<T, U>(val + base + lane, col + base + lane, 32, len, x, pol_s, pol_x);
+        if (SKIP && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+        store_row<T, ACC, ORD>(y, order, c * 32 + lane, n_rows, sum);
+        if (cn >= c1) break;
+        c = cn;
+        base = base_n;
+        w = w_n;
+        len = SKIP ? len_n : w_n;
+    }
 }
 
 // Chunk-list variant (multi-GPU interior / boundary passes): block b handles
@@ -373,6 +426,31 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(                      \
         m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0, \
         p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol)
+    // persistent sweep for short chunks (C = 32): SELLB_SWEEP=0/1 forces it
+    static const int sweep_env = [] {
+        const char* e = getenv("SELLB_SWEEP");
+        return e ? atoi(e) : -1;
+    }();
+    const bool sweep = CC == 32 && !n_long &&
+                       (sweep_env >= 0 ? sweep_env == 1 : m->max_cl <= 8);
+    if (sweep) {
+        static const int sms = [] {
+            int d = 0, n = 148;
+            cudaGetDevice(&d);
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+            return n;
+        }();
+        const int64_t chunks = (p1 - p0) / 32;
+        const int64_t blocks = std::min<int64_t>((chunks + 7) / 8, (int64_t)sms * 6);
+#define SELLB_SWEEP_LAUNCH(UU)                                                                   \
+    k_spmv_sell_sweep<T, SKIP, ACC, ORD, UU><<<(unsigned)blocks, kThreads, 0, st>>>(             \
+        m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, p0 / 32,   \
+        p1 / 32, m->n_rows, l2pol)
+        if (m->max_cl <= 6) SELLB_SWEEP_LAUNCH(6);
+        else SELLB_SWEEP_LAUNCH(8);
+#undef SELLB_SWEEP_LAUNCH
+        return 0;
+    }
     if (n_long) {
         if (u8) SELLB_LAUNCH(8, true, m->long_rows, n_long, m->long_th);
         else SELLB_LAUNCH(4, true, m->long_rows, n_long, m->long_th);
