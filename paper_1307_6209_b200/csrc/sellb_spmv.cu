@@ -426,13 +426,15 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(                      \
         m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0, \
         p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol)
-    // persistent sweep for short chunks (C = 32): SELLB_SWEEP=0/1 forces it
+    // persistent sweep for short chunks (C = 32): opt-in with SELLB_SWEEP=1.
+    // Measured slower than one warp per chunk (cfg1 455 vs 485 GF/s, cfg2
+    // 931 vs 1026): the 64-warp/SM one-shot grid already hides the metadata
+    // round trip, the sweep's extra registers cost occupancy.
     static const int sweep_env = [] {
         const char* e = getenv("SELLB_SWEEP");
-        return e ? atoi(e) : -1;
+        return e ? atoi(e) : 0;
     }();
-    const bool sweep = CC == 32 && !n_long &&
-                       (sweep_env >= 0 ? sweep_env == 1 : m->max_cl <= 8);
+    const bool sweep = CC == 32 && !n_long && sweep_env == 1;
     if (sweep) {
         static const int sms = [] {
             int d = 0, n = 148;
