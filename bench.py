@@ -263,6 +263,44 @@ def run_reference(args):
 # our arm
 # ---------------------------------------------------------------------------
 
+def model_block(s, nnz, n_rows, n_cols, n_pad, n_chunks, slots, s_v, traffic, kern_ms, peak):
+    """The paper's performance model next to the measurement (model.py):
+    beta, sector beta_eff, code balance with ideal alpha and the predicted
+    P = b/B, and -- when an ncu capture of this layout is committed -- the
+    measured balance and alpha from DRAM bytes."""
+    from paper_1307_6209_b200 import model
+    out = {"beta": round(nnz / slots, 6) if slots else 1.0}
+    try:
+        be, vs, cs_ = s.sector_occupancy()
+        out["beta_eff"] = round(be, 6)
+    except Exception:                      # imported without row lengths
+        vs = cs_ = None
+    if nnz and n_rows and n_cols and slots:
+        nzr, nzc = nnz / n_rows, nnz / n_cols
+        if s_v == 8:
+            bal = model.code_balance_sell(1.0 / nzc, nnz / slots, nzr)
+            out["B_paper_ideal_alpha"] = round(bal, 4)
+            out["P_paper_GFs"] = round(peak / bal, 1)
+        out["B_alg"] = round(model.algorithmic_bytes(nnz, n_cols, n_pad, n_chunks, s_v=s_v)
+                             / (2.0 * nnz), 4)
+        if traffic and s_v == 8:
+            out["B_measured"] = round(traffic / (2.0 * nnz), 4)
+            a = model.infer_alpha(traffic, nnz, nnz / slots, nzr, line_bytes=32)
+            out["alpha_paper"] = round(a.alpha, 4)
+            out["alpha_ideal"] = round(1.0 / nzc, 4)
+            if s.variant == "pad_incl":
+                mat, extra = 12 * slots, 0
+            elif vs is not None:
+                mat, extra = 32 * (vs + cs_), 4 * n_pad
+            else:
+                mat = None
+            if mat is not None:
+                out["alpha_eff"] = round(model.alpha_from_traffic(
+                    traffic, nnz, mat, n_pad, n_chunks, extra_bytes=extra).alpha, 4)
+            out["traffic_source"] = "profiles/ncu_traffic.json (ncu dram bytes, one launch)"
+    return out
+
+
 def load_profile_traffic(key):
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
@@ -288,6 +326,23 @@ def host_workload(args, dt_np):
     s = sb.crs_to_sell(crs, args.C, args.sigma, dtype=dt_np)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
+    # the device build alone (CRS already in HBM), timed with CUDA events
+    dev = torch.device("cuda", 0)
+    rpt_d = torch.from_numpy(crs.rpt).to(dev)
+    col_d = torch.from_numpy(crs.col).to(dev)
+    val_d = torch.from_numpy(crs.val.astype(dt_np)).to(dev)
+    sb.crs_to_sell_device(rpt_d, col_d, val_d, crs.n_rows, crs.n_cols, args.C, args.sigma).free()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sb.crs_to_sell_device(rpt_d, col_d, val_d, crs.n_rows, crs.n_cols, args.C, args.sigma).free()
+    e1.record()
+    e1.synchronize()
+    build_dev_ms = e0.elapsed_time(e1)
+    del rpt_d, col_d, val_d
+    t0 = time.perf_counter()
+    oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, args.C, args.sigma)
+    build_cpu_s = time.perf_counter() - t0
 
     def parity(yd):
         o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val.astype(dt_np), crs.n_rows,
@@ -304,7 +359,13 @@ def host_workload(args, dt_np):
         return {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": kind,
                 "sample": sample + f"; host {host_cpu_desc()}"}
 
-    return {"sell": s, "desc": desc, "x": x, "build_s": build_s, "parity": parity, "cpu": cpu}
+    return {"sell": s, "desc": desc, "x": x, "build_s": build_s, "parity": parity, "cpu": cpu,
+            "build": {"device_ms": round(build_dev_ms, 3),
+                      "host_to_sell_s": round(build_s, 4),
+                      "cpu_port_1thread_s": round(build_cpu_s, 4),
+                      "note": "device_ms: crs_to_sell on CRS already in HBM (CUDA events); "
+                              "host_to_sell_s adds the pageable H2D of the CRS; cpu: the C "
+                              "restatement of formats.py:295-393 (oracle), one thread"}}
 
 
 def cfg5_workload(args, dt_np):
@@ -492,7 +553,10 @@ def run_ours(args):
                           "SpMV's own events" % (4 * l2_bytes // 2**20)) if flush is not None
                    else "inputs larger than L2 (V_alg %.0f MB > %d MB L2)" % (
                        v_alg / 1e6, l2_bytes // 2**20),
-                   "build_s": round(build_s, 4), "parity_vs_oracle": parity},
+                   "build_s": round(build_s, 4), "build": wl.get("build"),
+                   "parity_vs_oracle": parity},
+        "model": model_block(s, nnz, n_rows, n_cols, n_pad, n_chunks, slots, s_v, traffic,
+                             kern_ms, peak),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "peak_source": f"{peak_kind} hbm_gbs (copy)",
