@@ -191,6 +191,12 @@ int sellb_l2_flush(void* scratch_dev, int64_t bytes, void* stream);
  * y[p] + 0*x0 (NaN); with finite *x0 the kernel writes nothing. */
 int sellb_pad_fixup(const sellb_mat* m, const void* x0, void* y, void* stream);
 
+/* Boundary classification for the row-partitioned path: chunk_flag[c] = 1
+ * iff some stored row p of chunk c has row_flag[order[p]] != 0 (row_flag in
+ * ORIGINAL row order, e.g. "reads a non-owned column"), else 0. */
+int sellb_chunk_flags(const sellb_mat* m, const uint8_t* row_flag, uint8_t* chunk_flag,
+                      void* stream);
+
 /* Halo pack / unpack for the row-partitioned multi-GPU SpMV (dist.py):
  * out[k] = x[idx[k]]  and  x[idx[k]] = in[k]  (k < n), on `stream`. */
 int sellb_gather(const void* x, const int32_t* idx, void* out, int64_t n, int32_t dtype,

@@ -33,7 +33,7 @@ EXPORTED = (
     "sellb_sector_occupancy", "sellb_read_sum", "sellb_copy", "sellb_l2_flush",
     "sellb_host_alloc", "sellb_host_free", "sellb_gather", "sellb_scatter",
     "sellb_pad_fixup", "sellb_gen_hamiltonian_rpt", "sellb_gen_hamiltonian_fill",
-    "sellb_export_range", "sellb_infer_row_lengths",
+    "sellb_export_range", "sellb_infer_row_lengths", "sellb_chunk_flags",
 )
 
 
@@ -100,6 +100,7 @@ _PROTOS = {
     "sellb_host_free": (ctypes.c_int, [_vp]),
     "sellb_export_range": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sellb_infer_row_lengths": (ctypes.c_int, [_vp, _vp]),
+    "sellb_chunk_flags": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
 }
 
 _lib = None

@@ -342,6 +342,23 @@ k_spmv_sell_list(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     y[p] = ACC ? Arith<T>::add(y[p], sum) : sum;
 }
 
+// chunk_flag[c] = OR over the chunk's stored rows of row_flag[original row]
+// (one warp per chunk)
+__global__ void k_chunk_flags(const int32_t* __restrict__ order, int64_t n_rows, int64_t n_chunks,
+                              int64_t C, const uint8_t* __restrict__ row_flag,
+                              uint8_t* __restrict__ chunk_flag) {
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= n_chunks) return;
+    int f = 0;
+    for (int64_t r = lane; r < C; r += 32) {
+        const int64_t o = order[c * C + r];
+        if (o < n_rows) f |= row_flag[o] != 0;
+    }
+    f = __any_sync(0xffffffffu, f);
+    if (lane == 0) chunk_flag[c] = (uint8_t)f;
+}
+
 // Padding fix-up for the row-partitioned path (see sellb_pad_fixup).
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
@@ -576,6 +593,22 @@ int sellb_spmv_chunk_list(const sellb_mat* m, const int32_t* chunk_ids, int64_t 
     if (!m || !y || (n_ids && !chunk_ids)) return set_error(SELLB_EPARAM, "NULL argument");
     DeviceGuard guard(m->device);
     return launch_spmv_list(m, chunk_ids, n_ids, x, y, accumulate, (cudaStream_t)stream);
+}
+
+int sellb_chunk_flags(const sellb_mat* m, const uint8_t* row_flag, uint8_t* chunk_flag,
+                      void* stream) {
+    clear_error();
+    if (!m || !row_flag || !chunk_flag) return set_error(SELLB_EPARAM, "NULL argument");
+    if (!m->order && m->n_rows) return set_error(SELLB_EPARAM, "matrix has no permutation");
+    if (m->n_chunks == 0) return 0;
+    DeviceGuard guard(m->device);
+    k_chunk_flags<<<(unsigned)grid_for(m->n_chunks * 32, kThreads), kThreads, 0,
+                    (cudaStream_t)stream>>>(m->order, m->n_rows, m->n_chunks, m->C, row_flag,
+                                            chunk_flag);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_error(SELLB_ERESOURCE, "chunk-flag launch failed: %s", cudaGetErrorString(e));
+    return 0;
 }
 
 int sellb_pad_fixup(const sellb_mat* m, const void* x0, void* y, void* stream) {

@@ -312,6 +312,59 @@ def setup(crs_local, bounds, C, sigma, rank, world, device, engine_factory,
                     group=group)
 
 
+def requests_torch(col_t, bounds, rank):
+    """HaloPlan.requests on a (device) torch tensor of local column indices:
+    sorted unique non-owned columns grouped by owner, computed where the
+    matrix lives (torch.unique / searchsorted on the GPU)."""
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    remote = torch.unique(col_t[(col_t < r0) | (col_t >= r1)])
+    if remote.numel() == 0:
+        return {}
+    b = torch.as_tensor(np.asarray(bounds, dtype=np.int64), device=col_t.device)
+    owner = torch.searchsorted(b, remote.to(torch.int64), right=True) - 1
+    out = {}
+    for p in torch.unique(owner).tolist():
+        if p != rank:
+            out[int(p)] = remote[owner == p].to(torch.int32).cpu().numpy()
+    return out
+
+
+def setup_device(rpt_t, col_t, val_t, n_global, bounds, C, sigma, rank, world, device,
+                 group=None, gathered=None):
+    """Row-partitioned setup for a block whose CRS is already in HBM (torch
+    tensors on `device`, global column indices): device build, halo plan and
+    interior/boundary split without a host copy of the block (cfg5: ~2 GB
+    of CRS per GPU at 8 GPUs).  ``gathered`` replaces the all_gather of the
+    request lists (single-process loopback tests)."""
+    from . import _lib
+    from .formats import crs_to_sell_device
+    n_local = rpt_t.numel() - 1
+    s = crs_to_sell_device(rpt_t, col_t, val_t, n_local, n_global, C, sigma,
+                           device=device.index or 0)
+    info = s.info()
+    has_padding = info.slots > info.nnz
+    if gathered is None:
+        plan_req = requests_torch(col_t, bounds, rank)
+        gathered = [None] * world
+        tdist.all_gather_object(gathered, (plan_req, bool(has_padding)), group=group)
+    plan = HaloPlan.from_requests(rank, world, bounds, gathered)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    remote = ((col_t < r0) | (col_t >= r1)).to(torch.int64)
+    cnt = torch.zeros(remote.numel() + 1, dtype=torch.int64, device=col_t.device)
+    torch.cumsum(remote, 0, out=cnt[1:])
+    row_flag = ((cnt[rpt_t[1:]] - cnt[rpt_t[:-1]]) > 0).to(torch.uint8).contiguous()
+    chunk_flag = torch.empty(info.n_chunks, dtype=torch.uint8, device=col_t.device)
+    _lib.check(_lib.load().sellb_chunk_flags(s.handle, row_flag.data_ptr(),
+                                             chunk_flag.data_ptr(),
+                                             torch.cuda.current_stream(device).cuda_stream))
+    bnd = chunk_flag.cpu().numpy().astype(bool)
+    del remote, cnt, row_flag
+    engine = CudaEngine(s, device)
+    tdt = torch.float32 if s.dtype == np.float32 else torch.float64
+    return DistSpmv(engine, plan, info.n_chunks, info.n_rows_padded, n_global, _runs(~bnd),
+                    _runs(bnd), has_padding, device, tdt, group=group)
+
+
 def cuda_engine_factory(C, sigma, device, dtype=None):
     """engine_factory for GPUs: device build of the local block."""
     from .formats import crs_to_sell
@@ -331,9 +384,23 @@ def cuda_engine_factory(C, sigma, device, dtype=None):
 # benchmark entry (torchrun, one process per GPU)
 # ---------------------------------------------------------------------------
 
+def _cfg5_bounds(n, world, C, sigma):
+    """Equal row blocks aligned to lcm(C, sigma_eff) (cfg5 rows carry ~19.7
+    entries each, so equal rows balance the nonzeros)."""
+    s_eff = sigma_effective(n, C, sigma) or 1
+    unit = C * s_eff // math.gcd(C, s_eff)
+    b = [min(n, int(round(n * k / world / unit)) * unit) for k in range(world)] + [n]
+    return np.array(b, dtype=np.int64)
+
+
 def bench_main(args):
-    """Weak scaling: the 27-point stencil on 128 x 128 x (128 N), one
-    128^3 z-slab per GPU, halo = one 128x128 plane per neighbour."""
+    """Multi-GPU benchmark under torchrun (one process per GPU, NCCL).
+
+    cfg2 (default) -- weak scaling: the 27-point stencil on 128 x 128 x
+    (128 N), one 128^3 z-slab per GPU, halo = one 128x128 plane per
+    neighbour.  cfg5 -- strong scaling: the N = 2^26 banded-random matrix
+    split into N row blocks, each generated and built on its own GPU, halo
+    over the +-2^20 hops."""
     import json
     import os
     import statistics
@@ -348,15 +415,31 @@ def bench_main(args):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     tdist.init_process_group("nccl", device_id=device)
-    n, nz_per = 128, 128
-    nz = nz_per * world
-    n_glob = n * n * nz
     C, sigma = 32, args.sigma
-    crs = generate.stencil27_slab(n, nz, rank * nz_per, (rank + 1) * nz_per)
-    bounds = np.arange(world + 1, dtype=np.int64) * (n * n * nz_per)
     t0 = time.perf_counter()
-    ds = setup(crs, bounds, C, sigma, rank, world, device,
-               cuda_engine_factory(C, sigma, device))
+    if args.config == "cfg5":
+        n_glob = args.n or (1 << 26)
+        bounds = _cfg5_bounds(n_glob, world, C, sigma)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        rpt_t, col_t, val_t = generate.hamiltonian_device(n_glob, r0, r1, device=local)
+        ds = setup_device(rpt_t, col_t, val_t, n_glob, bounds, C, sigma, rank, world, device)
+        del rpt_t, col_t, val_t
+        torch.cuda.empty_cache()
+        workload = (f"banded-random N={n_glob} (device-generated) in {world} row blocks, "
+                    f"SELL-32-{sigma}, NCCL halo")
+        scaling = "strong"
+        crs = None
+    else:
+        n, nz_per = 128, 128
+        nz = nz_per * world
+        n_glob = n * n * nz
+        crs = generate.stencil27_slab(n, nz, rank * nz_per, (rank + 1) * nz_per)
+        bounds = np.arange(world + 1, dtype=np.int64) * (n * n * nz_per)
+        ds = setup(crs, bounds, C, sigma, rank, world, device,
+                   cuda_engine_factory(C, sigma, device))
+        workload = (f"3D 27-point stencil 128x128x{nz} row-partitioned into {world} "
+                    f"z-slabs, SELL-32-{sigma}, NCCL halo")
+        scaling = "weak"
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     x_glob_rng = np.random.default_rng(12345)
@@ -364,15 +447,25 @@ def bench_main(args):
     ds.x_local.copy_(torch.from_numpy(x_all[ds.r0:ds.r1]))
     sell = ds.engine.sell
     nnz_local = sell.nnz
-    # parity of this rank's block against the oracle with the full x
+    n_rows_local = ds.r1 - ds.r0
+    # parity of this rank's block (cfg5: its first 65536 rows) against the
+    # oracle with the full x -- block builds equal slices
     parity = None
     if not args.skip_parity:
         import oracle
         ds.step()
         torch.cuda.synchronize()
-        o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, C, sigma)
+        if crs is None:
+            from .formats import CRSMatrix
+            blk = min(1 << 16, n_rows_local)
+            rp, cl_, vl = generate.hamiltonian_rows(n_glob, ds.r0, ds.r0 + blk)
+            crs_chk = CRSMatrix(blk, n_glob, rp, cl_, vl)
+        else:
+            crs_chk = crs
+        o = oracle.crs_to_sell(crs_chk.rpt, crs_chk.col, crs_chk.val, crs_chk.n_rows,
+                               crs_chk.n_cols, C, sigma)
         y_ref = oracle.spmv_sell(o, x_all, threads=max(1, (os.cpu_count() or 8) // world))
-        parity = bool(ds.y.cpu().numpy().tobytes() == y_ref.tobytes())
+        parity = bool(ds.y[:len(y_ref)].cpu().numpy().tobytes() == y_ref.tobytes())
     for _ in range(args.warmup):
         ds.step()
     torch.cuda.synchronize()
@@ -427,17 +520,16 @@ def bench_main(args):
         ms_max = float(t.item())
         nnz_tot = float(nz_t.item())
         value = 2.0 * nnz_tot * args.steps / (ms_max / 1e3) / 1e9
-        v_alg = algorithmic_bytes(nnz_local, crs.n_cols, sell.n_rows_padded, sell.n_chunks)
+        v_alg = algorithmic_bytes(nnz_local, n_glob, sell.n_rows_padded, sell.n_chunks)
         # x read once per rank means the owned slice + halo, not the global n_cols
-        v_alg = v_alg - 8 * crs.n_cols + 8 * (crs.n_rows + ds.plan.halo_entries())
+        v_alg = v_alg - 8 * n_glob + 8 * (n_rows_local + ds.plan.halo_entries())
         per_step_ms = ms_max / args.steps
         line = {
             "metric": "spMVM GFLOP/s (2*nnz/t), fp64 SELL-C-sigma", "value": round(value, 3),
             "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(per_step_ms, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"3D 27-point stencil 128x128x{nz} row-partitioned into "
-                                   f"{world} z-slabs, SELL-32-{sigma}, NCCL halo",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload,
                        "parallelism": f"row-blocks x{world}", "nnz": int(nnz_tot),
                        "halo_bytes_per_rank": ds.plan.bytes_per_step(),
                        "interior_ranges": len(ds.interior),
@@ -451,7 +543,7 @@ def bench_main(args):
                          "note": "per GPU, step time = max over ranks incl. exchange"},
             "e2e": {"value": round(2.0 * nnz_tot / float(e2e_s.item()) / 1e9, 3),
                     "unit": "GFLOP/s",
-                    "h2d_bytes_per_step": int(8 * crs.n_rows * world),
+                    "h2d_bytes_per_step": int(8 * n_glob),
                     "d2h_bytes_per_step": int(8 * sell.n_rows_padded * world),
                     "note": "per-rank pinned x slice in / y slice out each step, max over ranks"},
             "cpu_baseline": None,

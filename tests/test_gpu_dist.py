@@ -87,3 +87,32 @@ def test_blocks_equal_single_gpu(world, name, C, sigma):
             stitched = np.concatenate([ys[r][: int(bounds[r + 1] - bounds[r])]
                                        for r in range(world)])
             assert stitched.tobytes() == full[: m.n_rows].tobytes()
+
+
+def test_cfg5_device_setup_loopback():
+    """setup_device (device-resident CRS, torch-side halo plan, chunk flags
+    from sellb_chunk_flags) for 4 virtual ranks of the cfg5 generator; each
+    block's y equals the single-GPU product's slice."""
+    n, world, C, sigma = 1 << 20, 4, 32, 512
+    dev = torch.device("cuda", 0)
+    bounds = dist._cfg5_bounds(n, world, C, sigma)
+    blocks = [generate.hamiltonian_device(n, int(bounds[r]), int(bounds[r + 1]))
+              for r in range(world)]
+    gathered = [(dist.requests_torch(b[1], bounds, r), True) for r, b in enumerate(blocks)]
+    dss = [dist.setup_device(b[0], b[1], b[2], n, bounds, C, sigma, r, world, dev,
+                             gathered=gathered) for r, b in enumerate(blocks)]
+    rpt, col, val = generate.hamiltonian_device(n)
+    full = sb.crs_to_sell_device(rpt, col, val, n, n, C, sigma)
+    for x0 in (None, np.inf):
+        x = generate.rhs(n)
+        if x0 is not None:
+            x[0] = x0
+        ys = loopback_step(dss, x)
+        yf = sb.spmv_sell(full, x)
+        for r, y in enumerate(ys):
+            r0, r1 = int(bounds[r]), int(bounds[r + 1])
+            if x0 is None:
+                assert y[: r1 - r0].tobytes() == yf[r0:r1].tobytes(), r
+            else:
+                np.testing.assert_array_equal(y[: r1 - r0], yf[r0:r1])
+    assert all(len(ds.boundary) > 0 and len(ds.interior) > 0 for ds in dss)
