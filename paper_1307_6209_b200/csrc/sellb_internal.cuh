@@ -79,6 +79,11 @@ struct DeviceGuard {
     }
 };
 
+// Keep freed stream-ordered allocations in the device's default pool (the
+// default release threshold of 0 hands them back to the driver at every
+// synchronisation, turning each temporary into a fresh cudaMalloc).
+void retain_pool_memory();
+
 // RAII device buffer (stream-ordered free)
 struct DBuf {
     void* p = nullptr;
@@ -89,6 +94,7 @@ struct DBuf {
     ~DBuf() { if (p) cudaFreeAsync(p, s); }
     cudaError_t alloc(size_t bytes, cudaStream_t st) {
         s = st;
+        retain_pool_memory();
         return cudaMallocAsync(&p, bytes ? bytes : 16, st);
     }
     template <typename T> T* as() const { return static_cast<T*>(p); }
