@@ -8,6 +8,7 @@
 
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/sellb.h"
 
@@ -48,6 +49,9 @@ struct sellb_mat {
     void* x_buf = nullptr;
     void* y_buf = nullptr;
     std::mutex mu;
+    // host copy of cs (lazily fetched) for the TMA path's tile sizing
+    std::vector<int64_t> h_cs;
+    std::mutex hcs_mu;
     // pipelined host path: x pieces H2D / row blocks / y pieces D2H overlap
     static constexpr int kPipe = 16;
     bool pipe_ready = false;
@@ -109,6 +113,9 @@ int launch_spmv_list(const sellb_mat* m, const int32_t* ids, int64_t n_ids, cons
 int launch_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val, int32_t dtype,
                     const void* x, void* y, int64_t r0, int64_t r1, int accumulate,
                     int unrolled, cudaStream_t st);
+// sellb_tma.cu: returns 1 if launched, 0 if the layout does not qualify
+int launch_spmv_tma(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
+                    int accumulate, cudaStream_t st, const int64_t* h_cs);
 
 inline int64_t grid_for(int64_t n, int threads) { return (n + threads - 1) / threads; }
 

@@ -519,6 +519,30 @@ int launch_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t 
     if (out_order == SELLB_ORDER_ORIGINAL && !m->order)
         return set_error(SELLB_EPARAM, "original-order output needs the row permutation");
     if (c0 == c1) return 0;
+    // TMA bulk-copy path (sellb_tma.cu) for C = 32 pad-inclusive layouts
+    static const int tma_env = [] {
+        const char* e = getenv("SELLB_TMA");
+        return e ? atoi(e) : 0;
+    }();
+    if (tma_env == 1 && m->C == 32 && m->variant == SELLB_VARIANT_PAD_INCL &&
+        out_order == SELLB_ORDER_STORED && !m->n_long) {
+        sellb_mat* mm = const_cast<sellb_mat*>(m);
+        if ((int64_t)mm->h_cs.size() != m->n_chunks + 1) {
+            std::lock_guard<std::mutex> lk(mm->hcs_mu);
+            if ((int64_t)mm->h_cs.size() != m->n_chunks + 1) {
+                std::vector<int64_t> h(m->n_chunks + 1);
+                SELLB_CU(cudaMemcpy(h.data(), m->cs, h.size() * 8, cudaMemcpyDeviceToHost));
+                mm->h_cs.swap(h);
+            }
+        }
+        if (launch_spmv_tma(m, x, y, c0, c1, accumulate, st, mm->h_cs.data())) {
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess)
+                return set_error(SELLB_ERESOURCE, "tma spmv launch failed: %s",
+                                 cudaGetErrorString(e));
+            return 0;
+        }
+    }
     int rc = m->dtype == SELLB_F32
                  ? dispatch_sell<float>(m, x, y, c0 * m->C, c1 * m->C, accumulate, out_order, st)
                  : dispatch_sell<double>(m, x, y, c0 * m->C, c1 * m->C, accumulate, out_order, st);
