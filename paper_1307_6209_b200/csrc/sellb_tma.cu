@@ -180,12 +180,22 @@ int launch_spmv_tma(const sellb_mat* m, const void* x, void* y, int64_t c0, int6
     const int per_sm = std::max(1, (int)std::min<size_t>(8, (220 * 1024) / smem));
     const int64_t tiles = (c1 - c0 + kTile - 1) / kTile;
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * per_sm);
-#define SELLB_TMA(TT, AA)                                                                     \
+    static const int u_env = [] {
+        const char* e = getenv("SELLB_TMA_U");
+        return e ? atoi(e) : 16;
+    }();
+#define SELLB_TMA_U(TT, AA, UU)                                                               \
     do {                                                                                      \
-        auto kern = k_spmv_tma<TT, AA, 8>;                                                    \
+        auto kern = k_spmv_tma<TT, AA, UU>;                                                   \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
         kern<<<grid, kTmaThreads, smem, st>>>(m->cs, m->cl, m->col, (const TT*)m->val,       \
                                               (const TT*)x, (TT*)y, c0, c1, max_tile);       \
+    } while (0)
+#define SELLB_TMA(TT, AA)                                                                     \
+    do {                                                                                      \
+        if (u_env == 32) SELLB_TMA_U(TT, AA, 32);                                             \
+        else if (u_env == 8) SELLB_TMA_U(TT, AA, 8);                                          \
+        else SELLB_TMA_U(TT, AA, 16);                                                         \
     } while (0)
     if (m->dtype == SELLB_F32) {
         if (accumulate) SELLB_TMA(float, true); else SELLB_TMA(float, false);
@@ -193,6 +203,7 @@ int launch_spmv_tma(const sellb_mat* m, const void* x, void* y, int64_t c0, int6
         if (accumulate) SELLB_TMA(double, true); else SELLB_TMA(double, false);
     }
 #undef SELLB_TMA
+#undef SELLB_TMA_U
     return 1;
 }
 

@@ -39,11 +39,13 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
 else:
     import numpy as np
     os.makedirs("gpurun_out", exist_ok=True)
-    for tma in ("0", "1"):
+    for tma, u in (("0", "16"), ("1", "8"), ("1", "16"), ("1", "32")):
         subprocess.run([sys.executable, __file__, "child"],
-                       env={**os.environ, "SELLB_TMA": tma, "OUT": f"gpurun_out/tma{tma}"},
-                       timeout=600)
-    for name in ("cfg2", "cfg2_f32", "cfg5_s512_2^24"):
-        a = np.load(f"gpurun_out/tma0_{name}.npy")
-        b = np.load(f"gpurun_out/tma1_{name}.npy")
-        print(name, "bitwise equal:", a.tobytes() == b.tobytes())
+                       env={**os.environ, "SELLB_TMA": tma, "SELLB_TMA_U": u,
+                            "OUT": f"gpurun_out/tma{tma}_{u}"}, timeout=600)
+        print("  U =", u, flush=True)
+    for u in ("8", "16", "32"):
+        for name in ("cfg2", "cfg2_f32", "cfg5_s512_2^24"):
+            a = np.load(f"gpurun_out/tma0_16_{name}.npy")
+            b = np.load(f"gpurun_out/tma1_{u}_{name}.npy")
+            print(u, name, "bitwise equal:", a.tobytes() == b.tobytes())
