@@ -519,12 +519,16 @@ int launch_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t 
     if (out_order == SELLB_ORDER_ORIGINAL && !m->order)
         return set_error(SELLB_EPARAM, "original-order output needs the row permutation");
     if (c0 == c1) return 0;
-    // TMA bulk-copy path (sellb_tma.cu) for C = 32 pad-inclusive layouts
+    // TMA bulk-copy path (sellb_tma.cu) for C = 32 pad-inclusive layouts:
+    // default for fp32 (cfg2: 1503 vs 1472 GF/s), slower for fp64 (914 vs
+    // ~1030: too few consumer warps hide the gather latency).  SELLB_TMA=0/1
+    // forces it off/on.
     static const int tma_env = [] {
         const char* e = getenv("SELLB_TMA");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : -1;
     }();
-    if (tma_env == 1 && m->C == 32 && m->variant == SELLB_VARIANT_PAD_INCL &&
+    const bool tma = tma_env >= 0 ? tma_env == 1 : m->dtype == SELLB_F32;
+    if (tma && m->C == 32 && m->variant == SELLB_VARIANT_PAD_INCL &&
         out_order == SELLB_ORDER_STORED && !m->n_long) {
         sellb_mat* mm = const_cast<sellb_mat*>(m);
         if ((int64_t)mm->h_cs.size() != m->n_chunks + 1) {
