@@ -351,3 +351,36 @@ def test_pipelined_host_path_matches_device(cfg2):
     y_host = sb.spmv_sell(s, x)                       # pipelined host path
     y_dev = sb.spmv_sell(s, torch.from_numpy(x).cuda()).cpu().numpy()
     assert y_host.tobytes() == y_dev.tobytes()
+
+
+def test_tma_path_forced_bitwise():
+    """The TMA bulk-copy kernel (sellb_tma.cu) forced on for fp64 too (the
+    switch is read once per process, so in a child process): overwrite and
+    accumulate results equal the oracle bit for bit."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+import oracle, paper_1307_6209_b200 as sb
+from paper_1307_6209_b200 import generate
+m = generate.stencil27(24)
+for dt in (np.float64, np.float32):
+    s = sb.crs_to_sell(m, 32, 1, dtype=dt)
+    assert s.variant == "pad_incl"
+    o = oracle.crs_to_sell(m.rpt, m.col, m.val.astype(dt), m.n_rows, m.n_cols, 32, 1)
+    x = generate.rhs(m.n_cols, dtype=dt)
+    assert sb.spmv_sell(s, x).tobytes() == oracle.spmv_sell(o, x).tobytes()
+    y0 = np.linspace(-1, 1, s.n_rows_padded).astype(dt)
+    ya = sb.spmv_sell(s, x, y=y0.copy(), accumulate=True)
+    yr = y0.copy()
+    oracle.spmv_sell_range(o.cs, o.cl, 32, o.col, o.val, x, yr, 0, o.n_chunks, True)
+    assert ya.tobytes() == yr.tobytes()
+print("ok")
+'''
+    import os
+    env = dict(os.environ, SELLB_TMA="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                         timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
