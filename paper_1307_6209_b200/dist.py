@@ -403,7 +403,7 @@ def bench_main(args):
     over the +-2^20 hops."""
     import json
     import os
-    import statistics
+
     import time
 
     from . import generate

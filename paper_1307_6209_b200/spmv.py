@@ -20,7 +20,6 @@ Inputs may also be CUDA tensors (torch): then x/y stay on the device and
 nothing crosses PCIe.
 """
 
-import ctypes
 
 import numpy as np
 

@@ -36,7 +36,7 @@ def matrices():
 
 
 def run(out_json, timed=False):
-    import numpy as np
+
     import torch
     import paper_1307_6209_b200 as sb
     from paper_1307_6209_b200 import generate
