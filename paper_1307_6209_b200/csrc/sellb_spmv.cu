@@ -84,9 +84,24 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
     return v;
 }
 // RHS gather: read-only path, keep in L2
+// SELLB_XLD selects the gather's cache qualifiers at build time (A/B builds,
+// tools/build_variant.sh): 0 read-only path (default), 1 read-only without
+// L1 allocation, 2 plain coherent load, 3 read-only with L1 evict_last.
+#ifndef SELLB_XLD
+#define SELLB_XLD 0
+#endif
+#if SELLB_XLD == 1
+#define SELLB_XLD_Q "ld.global.nc.L1::no_allocate.L2::cache_hint"
+#elif SELLB_XLD == 2
+#define SELLB_XLD_Q "ld.global.L2::cache_hint"
+#elif SELLB_XLD == 3
+#define SELLB_XLD_Q "ld.global.nc.L1::evict_last.L2::cache_hint"
+#else
+#define SELLB_XLD_Q "ld.global.nc.L2::cache_hint"
+#endif
 __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
     double v;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    asm(SELLB_XLD_Q ".f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ float ld_x(const float* p, uint64_t pol) {
