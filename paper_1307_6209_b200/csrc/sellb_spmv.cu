@@ -454,10 +454,25 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     const bool u8 = u_env ? u_env == 8
                           : (sizeof(T) == 4 || m->max_cl > 64 ||
                              (m->n_rows > 0 && m->nnz >= 24 * m->n_rows));
+    // L1/shared carve-out: SELLB_CARVEOUT=<percent shared> (A/B knob; -1 = driver default)
+    static const int carve = [] {
+        const char* e = getenv("SELLB_CARVEOUT");
+        return e ? atoi(e) : -1;
+    }();
 #define SELLB_LAUNCH(UU, LL, LR, NL, TH)                                                        \
-    k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(                      \
-        m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C, p0, \
-        p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol)
+    do {                                                                                        \
+        if (carve >= 0) {                                                                       \
+            static bool set_ = false;                                                           \
+            if (!set_) {                                                                        \
+                cudaFuncSetAttribute(k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL>,                \
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve);    \
+                set_ = true;                                                                    \
+            }                                                                                   \
+        }                                                                                       \
+        k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(                  \
+            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,  \
+            p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol);                                 \
+    } while (0)
     // persistent sweep for short chunks (C = 32): opt-in with SELLB_SWEEP=1.
     // Measured slower than one warp per chunk (cfg1 455 vs 485 GF/s, cfg2
     // 931 vs 1026): the 64-warp/SM one-shot grid already hides the metadata
