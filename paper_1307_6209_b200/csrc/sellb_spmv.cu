@@ -181,7 +181,7 @@ __device__ __forceinline__ T row_sum(const T* __restrict__ vp, const int32_t* __
 // never be -0.0), so the chain needs no predicate.  kSeg*32 slots per batch;
 // the next batch's val/col loads are issued before the current batch's
 // gathers and add chain, so the DRAM round trip overlaps the chain.
-constexpr int kSeg = 8;
+constexpr int kSeg = 4;
 
 template <typename T, bool ACC, int ORD>
 __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
