@@ -178,9 +178,7 @@ __device__ __forceinline__ T row_sum(const T* __restrict__ vp, const int32_t* __
 // the same sequence of roundings as the reference's per-row loop, so the
 // result is bitwise identical.  Slots past the row length stage +0.0, and
 // adding +0.0 to a sum that started at +0.0 is an exact no-op (the sum can
-// never be -0.0), so the chain needs no predicate.  kSeg*32 slots per batch;
-// the next batch's val/col loads are issued before the current batch's
-// gathers and add chain, so the DRAM round trip overlaps the chain.
+// never be -0.0), so the chain needs no predicate.  kSeg*32 slots per batch.
 constexpr int kSeg = 4;
 
 template <typename T, bool ACC, int ORD>
@@ -199,38 +197,18 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
     const T* vp = val + base;
     const int32_t* cp = col + base;
     T sum = T(0);
-    T vn[kSeg];
-    int32_t cn[kSeg];
-#pragma unroll
-    for (int s = 0; s < kSeg; ++s) {          // batch 0
-        const int j = s * 32 + lane;
-        vn[s] = T(0);
-        cn[s] = 0;
-        if (j < len) {
-            vn[s] = ld_stream(vp + (int64_t)j * C, pol_s);
-            cn[s] = ld_stream(cp + (int64_t)j * C, pol_s);
-        }
-    }
     for (int j0 = 0; j0 < len; j0 += 32 * kSeg) {
         T prod[kSeg];
         int32_t c[kSeg];
         T v[kSeg];
 #pragma unroll
         for (int s = 0; s < kSeg; ++s) {
-            v[s] = vn[s];
-            c[s] = cn[s];
-        }
-        const int jn = j0 + 32 * kSeg;
-        if (jn < len) {                        // prefetch the next batch
-#pragma unroll
-            for (int s = 0; s < kSeg; ++s) {
-                const int j = jn + s * 32 + lane;
-                vn[s] = T(0);
-                cn[s] = 0;
-                if (j < len) {
-                    vn[s] = ld_stream(vp + (int64_t)j * C, pol_s);
-                    cn[s] = ld_stream(cp + (int64_t)j * C, pol_s);
-                }
+            const int j = j0 + s * 32 + lane;
+            v[s] = T(0);
+            c[s] = 0;
+            if (j < len) {
+                v[s] = ld_stream(vp + (int64_t)j * C, pol_s);
+                c[s] = ld_stream(cp + (int64_t)j * C, pol_s);
             }
         }
 #pragma unroll
