@@ -12,11 +12,13 @@
 // streams are marked L1::no_allocate with an L2 evict-first policy so they do
 // not push x out of the 126 MB L2.
 //
-// Bitwise parity with the reference: each row is summed by exactly one thread,
-// from +0.0, in ascending slot order, with separately rounded multiply and
-// add (__dmul_rn / __dadd_rn: no FMA contraction; the compiled reference has
-// none either).  Loads are batched U slots at a time for memory-level
-// parallelism, but the adds are issued in slot order.
+// Bitwise parity with the reference: each row is summed from +0.0, in
+// ascending slot order, with separately rounded multiply and add (__dmul_rn /
+// __dadd_rn: no FMA contraction; the compiled reference has none either) --
+// by one thread in the bulk role, or, for very long rows, by a warp that
+// first stages the rounded products and then adds them in order.  Loads are
+// batched U slots at a time for memory-level parallelism, but the adds are
+// issued in slot order.
 //
 // Padding: the PAD_SKIP variant stops each thread at its own row length (the
 // paper's "Sliced ELLR-T, T=1" optimisation).  The reference adds
