@@ -1,0 +1,114 @@
+"""Direct C-ABI entry points not exercised through the Python API elsewhere:
+the stateless reference-signature range kernel, device CRS kernels, the
+membench kernels, and int64 slot offsets beyond 2^31."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1307_6209_b200 as sb
+from paper_1307_6209_b200 import _lib, generate, kernels_cuda
+from conftest import case_id, golden_cases, load_case
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not sb.HAS_CUDA:
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("path", golden_cases()[::4], ids=case_id)
+def test_stateless_reference_signature(path):
+    """sellb_spmv_sell_range_host: _kernels.pyx:65-68 arguments on host arrays."""
+    g = load_case(path)
+    lib = _lib.load()
+    n = g["n_chunks"]
+    for acc, y0, want in ((0, np.zeros(g["n_rows_padded"]), g["y"]),
+                          (1, g["y0"].copy(), g["y_acc"])):
+        y = y0.copy()
+        _lib.check(lib.sellb_spmv_sell_range_host(
+            _lib.ptr(g["cs"]), _lib.ptr(g["cl"]), g["C"], _lib.ptr(g["col"]),
+            _lib.ptr(g["val"]), len(g["val"]), n, _lib.ptr(g["x"]), len(g["x"]),
+            _lib.ptr(y), len(y), 0, n, acc, 0))
+        assert y.tobytes() == want.tobytes()
+
+
+def test_stateless_signature_rejects_bad_range():
+    g = load_case(golden_cases()[0])
+    lib = _lib.load()
+    y = np.zeros(g["n_rows_padded"])
+    rc = lib.sellb_spmv_sell_range_host(
+        _lib.ptr(g["cs"]), _lib.ptr(g["cl"]), g["C"], _lib.ptr(g["col"]), _lib.ptr(g["val"]),
+        len(g["val"]), g["n_chunks"], _lib.ptr(g["x"]), len(g["x"]), _lib.ptr(y), len(y),
+        0, g["n_chunks"] + 1, 0, 0)
+    assert rc == -1
+
+
+def test_device_crs_entry():
+    """sellb_spmv_crs on device arrays == the reference CRS kernels bitwise."""
+    import torch
+    m = generate.powerlaw(50_000, seed=6, band=3000)
+    x = generate.rhs(m.n_cols)
+    t = {k: torch.from_numpy(v).cuda() for k, v in
+         (("rpt", m.rpt), ("col", m.col), ("val", m.val), ("x", x))}
+    lib = _lib.load()
+    for unrolled in (0, 1):
+        y = torch.zeros(m.n_rows, dtype=torch.float64, device="cuda")
+        _lib.check(lib.sellb_spmv_crs(t["rpt"].data_ptr(), t["col"].data_ptr(),
+                                      t["val"].data_ptr(), _lib.SELLB_F64, t["x"].data_ptr(),
+                                      y.data_ptr(), 0, m.n_rows, 0, unrolled,
+                                      torch.cuda.current_stream().cuda_stream))
+        ref = oracle.spmv_crs(m.rpt, m.col, m.val, x, m.n_rows, unrolled=bool(unrolled))
+        assert y.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_membench_kernels():
+    a = np.random.default_rng(1).uniform(-1, 1, 1_000_003)
+    assert kernels_cuda.read_sum(a) == pytest.approx(float(np.sum(a)), rel=1e-12, abs=1e-9)
+    dst = np.zeros_like(a)
+    kernels_cuda.copy_array(a, dst)
+    assert dst.tobytes() == a.tobytes()
+    from paper_1307_6209_b200 import membench
+    r = membench.microbench_read_sum(n_bytes=256 << 20, reps=3)
+    c = membench.microbench_copy(n_bytes=256 << 20, reps=3)
+    assert r.gbps > 1000 and c.gbps > 1000
+
+
+def test_lru_not_provided():
+    with pytest.raises(sb.ResourceError):
+        kernels_cuda.lru_stream_misses(np.zeros(3, np.int64), 2, 4)
+
+
+def test_int64_offsets_beyond_2p31_slots():
+    """2^27-row cfg5-style matrix: > 2^31 stored slots (int64 cs and flat
+    offsets end to end); sampled blocks bit-exact against the oracle."""
+    import gc
+    import torch
+    n = 1 << 27
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100 << 30:
+        pytest.skip("needs ~100 GB of free device memory")
+    rpt, col, val = generate.hamiltonian_device(n)
+    s = sb.crs_to_sell_device(rpt, col, val, n, n, 32, 1)
+    del rpt, col, val
+    gc.collect()
+    torch.cuda.empty_cache()
+    info = s.info()
+    assert info.slots > 2 ** 31 and info.nnz > 2 ** 31
+    x = generate.rhs(n)
+    xd = torch.from_numpy(x).cuda()
+    y = sb.spmv_sell(s, xd).cpu().numpy()
+    for r0 in (0, n // 2, n - 4096):
+        rp, cl_, vl = generate.hamiltonian_rows(n, r0, r0 + 4096)
+        o = oracle.crs_to_sell(rp, cl_, vl, 4096, n, 32, 1)
+        got = s.export_range(r0 // 32, (r0 + 4096) // 32)
+        for k in ("cs", "cl", "col", "val", "row_lengths"):
+            assert got[k].tobytes() == getattr(o, k).tobytes(), k
+        assert y[r0:r0 + 4096].tobytes() == oracle.spmv_sell(o, x).tobytes()
+    s.free()
+    del xd
+    torch.cuda.empty_cache()
