@@ -425,10 +425,10 @@ def run_ours(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
-        from paper_1307_6209_b200 import dist
+        import bench_dist
         args.peak = measured_peaks()[0]
         args.clock_sampler = ClockSampler
-        return dist.bench_main(args)
+        return bench_dist.bench_main(args)
     import oracle
     import paper_1307_6209_b200 as sb
     from paper_1307_6209_b200 import _lib
