@@ -424,7 +424,7 @@ def cfg5_workload(args, dt_np):
 def run_ours(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or os.environ.get("SELLB_FORCE_DIST"):   # (1-rank smoke of the N>1 leg)
         import bench_dist
         args.peak = measured_peaks()[0]
         args.clock_sampler = ClockSampler
