@@ -471,10 +471,53 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
                 set_ = true;                                                                    \
             }                                                                                   \
         }                                                                                       \
-        k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(                  \
-            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,  \
-            p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol);                                 \
+        if (persist) {                                                                          \
+            cudaLaunchConfig_t cfg_{};                                                          \
+            cfg_.gridDim = dim3(grid);                                                          \
+            cfg_.blockDim = dim3(kThreads);                                                     \
+            cfg_.stream = st;                                                                   \
+            cudaLaunchAttribute at_[1];                                                         \
+            at_[0].id = cudaLaunchAttributeAccessPolicyWindow;                                  \
+            at_[0].val.accessPolicyWindow = apw;                                                \
+            cfg_.attrs = at_;                                                                   \
+            cfg_.numAttrs = 1;                                                                  \
+            cudaLaunchKernelEx(&cfg_, k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL>, m->cs, m->cl,  \
+                               m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,  \
+                               m->C, p0, p1, m->n_rows, (const int32_t*)(LR), (int64_t)(NL),   \
+                               (int)(TH), (const int32_t*)m->chunk_th, l2pol);                  \
+        } else {                                                                                \
+            k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(              \
+                m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
+                m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol);                       \
+        }                                                                                       \
     } while (0)
+    // x as a persisting L2 window (SELLB_L2PERSIST=1, A/B knob): the driver
+    // sets aside up to the device's persisting-L2 maximum for it
+    static const int persist_env = [] {
+        const char* e = getenv("SELLB_L2PERSIST");
+        return e ? atoi(e) : 0;
+    }();
+    const bool persist = persist_env == 1;
+    cudaAccessPolicyWindow apw{};
+    if (persist) {
+        static size_t max_persist = [] {
+            int d = 0, v = 0;
+            cudaGetDevice(&d);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, d);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v);
+            return (size_t)v;
+        }();
+        int dmax = 0, d = 0;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&dmax, cudaDevAttrMaxAccessPolicyWindowSize, d);
+        const size_t xbytes = (size_t)m->n_cols * sizeof(T);
+        apw.base_ptr = const_cast<void*>(x);
+        apw.num_bytes = std::min<size_t>(xbytes, (size_t)dmax);
+        apw.hitRatio = apw.num_bytes ? std::min(1.0f, (float)max_persist / (float)apw.num_bytes)
+                                     : 0.f;
+        apw.hitProp = cudaAccessPropertyPersisting;
+        apw.missProp = cudaAccessPropertyStreaming;
+    }
     // persistent sweep for short chunks (C = 32): opt-in with SELLB_SWEEP=1.
     // Measured slower than one warp per chunk (cfg1 455 vs 485 GF/s, cfg2
     // 931 vs 1026): the 64-warp/SM one-shot grid already hides the metadata
