@@ -214,6 +214,20 @@ int sellb_gen_hamiltonian_fill(int64_t n, int64_t r0, int64_t r1, const int64_t*
                                int32_t n_off, double keep, uint64_t seed, const int64_t* rpt_dev,
                                int32_t* col_dev, void* val_dev, int32_t dtype, void* stream);
 
+/* COO -> canonical CRS on the device: the step before the build
+ * (SURVEY.md §8(f)3).  Replaces COOMatrix's bounds check (formats.py:50-70),
+ * canonicalize_coo (formats.py:89-108) and coo_to_crs (formats.py:169-175).
+ * rows/cols int64[nnz], vals f64[nnz] in any order with duplicates; outputs
+ * rpt int64[n_rows+1], col int32[cap nnz], val f64[cap nnz] and *nnz_out =
+ * the number of distinct coordinates.  Duplicates are summed exactly as the
+ * reference's np.add.reduceat (first entry + NumPy pairwise sum of the rest,
+ * in stable (row, col) order): bit-identical output.  Host or device
+ * pointers (ptrs_on_device); -3 with the reference's message for an
+ * out-of-range index. */
+int sellb_coo_to_crs(const int64_t* rows, const int64_t* cols, const double* vals, int64_t nnz,
+                     int64_t n_rows, int64_t n_cols, int64_t* rpt, int32_t* col, double* val,
+                     int64_t* nnz_out, int32_t device, void* stream, int32_t ptrs_on_device);
+
 /* Pinned host buffers for the end-to-end path. */
 int sellb_host_alloc(size_t bytes, void** out);
 int sellb_host_free(void* p);

@@ -79,6 +79,9 @@ def lib():
                           ctypes.c_int]
         L.oracle_read_sum.restype = ctypes.c_double
         L.oracle_read_sum.argtypes = [_f64p, _i64]
+        L.oracle_coo_to_crs.restype = _i64
+        L.oracle_coo_to_crs.argtypes = [_i64p, _i64p, _f64p, _i64, _i64, _i64p, _i32p,
+                                        _f64p]
         _lib = L
     return _lib
 
@@ -101,6 +104,23 @@ class OracleSell:
     @property
     def stored_slots(self):
         return int(self.cs[-1])
+
+
+def coo_to_crs(rows, cols, vals, n_rows):
+    """canonicalize_coo + coo_to_crs (formats.py:89-108,169-175): returns
+    (rpt int64, col int32, val f64).  Indices must be in bounds."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    cols = np.ascontiguousarray(cols, np.int64)
+    vals = np.ascontiguousarray(vals, np.float64)
+    nnz = len(vals)
+    rpt = np.zeros(n_rows + 1, np.int64)
+    col = np.zeros(max(nnz, 1), np.int32)
+    val = np.zeros(max(nnz, 1))
+    u = lib().oracle_coo_to_crs(_p(rows, _i64p), _p(cols, _i64p), _p(vals, _f64p), nnz,
+                                n_rows, _p(rpt, _i64p), _p(col, _i32p), _p(val, _f64p))
+    if u < 0:
+        raise MemoryError("oracle_coo_to_crs")
+    return rpt, col[:u].copy(), val[:u].copy()
 
 
 def sigma_eff(n_rows, C, sigma):

@@ -300,3 +300,87 @@ double oracle_read_sum(const double *a, int64_t n)
     while (i < n) { rest += a[i]; ++i; }
     return (((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7))) + rest;
 }
+
+/* ---------------------------------------------------------------------- */
+/* canonicalize_coo + coo_to_crs: formats.py:89-108, 169-175.              */
+/* Order: np.lexsort((cols, rows)) = stable sort by (row, col).  Runs of   */
+/* equal coordinates are summed like np.add.reduceat: the run's first      */
+/* value plus NumPy's pairwise_sum of the rest (restated below: < 8 terms  */
+/* sequentially from -0.0; <= 128 terms in eight interleaved partial sums, */
+/* combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail; longer     */
+/* runs split at n/2 rounded down to a multiple of 8).                     */
+/* ---------------------------------------------------------------------- */
+
+static const int64_t *g_r, *g_c;   /* sort keys (single-threaded oracle) */
+
+static int key_less(int64_t a, int64_t b)
+{
+    return g_r[a] < g_r[b] || (g_r[a] == g_r[b] && g_c[a] < g_c[b]);
+}
+
+static void msort_key(int64_t *a, int64_t *tmp, int64_t lo, int64_t hi)
+{
+    if (hi - lo < 2) return;
+    int64_t mid = lo + (hi - lo) / 2;
+    msort_key(a, tmp, lo, mid);
+    msort_key(a, tmp, mid, hi);
+    int64_t i = lo, j = mid, k = lo;
+    while (i < mid && j < hi) tmp[k++] = key_less(a[j], a[i]) ? a[j++] : a[i++];
+    while (i < mid) tmp[k++] = a[i++];
+    while (j < hi) tmp[k++] = a[j++];
+    memcpy(a + lo, tmp + lo, (size_t)(hi - lo) * sizeof(int64_t));
+}
+
+static double np_pairwise(const double *v, const int64_t *ord, int64_t n)
+{
+    if (n < 8) {
+        double r = -0.0;
+        for (int64_t i = 0; i < n; ++i) r += v[ord[i]];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        int64_t i;
+        for (int j = 0; j < 8; ++j) r[j] = v[ord[j]];
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += v[ord[i + j]];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += v[ord[i]];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise(v, ord, n2) + np_pairwise(v, ord + n2, n - n2);
+}
+
+/* Inputs must be in bounds (the COOMatrix constructor checks).  Writes rpt
+ * [n_rows+1], col/val [<= nnz]; returns the canonical nnz, or -1. */
+int64_t oracle_coo_to_crs(const int64_t *rows, const int64_t *cols, const double *vals,
+                          int64_t nnz, int64_t n_rows, int64_t *rpt, int32_t *col,
+                          double *val)
+{
+    int64_t *ord = malloc((size_t)(nnz ? nnz : 1) * sizeof(int64_t));
+    int64_t *tmp = malloc((size_t)(nnz ? nnz : 1) * sizeof(int64_t));
+    if (!ord || !tmp) { free(ord); free(tmp); return -1; }
+    for (int64_t i = 0; i < nnz; ++i) ord[i] = i;
+    g_r = rows; g_c = cols;
+    msort_key(ord, tmp, 0, nnz);
+    int64_t u = 0;
+    for (int64_t s = 0; s < nnz;) {
+        int64_t e = s + 1;
+        while (e < nnz && rows[ord[e]] == rows[ord[s]] && cols[ord[e]] == cols[ord[s]]) ++e;
+        double v = vals[ord[s]];
+        if (e - s > 1) v = v + np_pairwise(vals, ord + s + 1, e - s - 1);
+        col[u] = (int32_t)cols[ord[s]];
+        val[u] = v;
+        tmp[u] = rows[ord[s]];          /* row of unique entry u */
+        ++u;
+        s = e;
+    }
+    /* rpt = cumsum(bincount(rows, minlength=n_rows)), formats.py:171-173 */
+    for (int64_t r = 0; r <= n_rows; ++r) rpt[r] = 0;
+    for (int64_t k = 0; k < u; ++k) rpt[tmp[k] + 1] += 1;
+    for (int64_t r = 0; r < n_rows; ++r) rpt[r + 1] += rpt[r];
+    free(ord); free(tmp);
+    return u;
+}

@@ -34,6 +34,7 @@ EXPORTED = (
     "sellb_host_alloc", "sellb_host_free", "sellb_gather", "sellb_scatter",
     "sellb_pad_fixup", "sellb_gen_hamiltonian_rpt", "sellb_gen_hamiltonian_fill",
     "sellb_export_range", "sellb_infer_row_lengths", "sellb_chunk_flags",
+    "sellb_coo_to_crs",
 )
 
 
@@ -101,6 +102,8 @@ _PROTOS = {
     "sellb_export_range": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sellb_infer_row_lengths": (ctypes.c_int, [_vp, _vp]),
     "sellb_chunk_flags": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "sellb_coo_to_crs": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
+                                        ctypes.POINTER(_i64), _i32, _vp, _i32]),
 }
 
 _lib = None

@@ -149,12 +149,98 @@ class CRSMatrix:
         return np.diff(self.rpt)
 
 
-def coo_to_crs(m):
-    """formats.py:169-175."""
+def coo_to_crs(m, *, device=None, stream=None):
+    """formats.py:169-175.
+
+    ``device=None`` keeps the reference's host conversion; ``device=k`` runs
+    the canonicalisation on GPU k (``sellb_coo_to_crs``, csrc/sellb_coo.cu)
+    and returns the same CRSMatrix bit for bit (duplicate sums included)."""
+    if device is not None:
+        lib = _lib.require_device()
+        rpt = np.zeros(m.n_rows + 1, dtype=OFFSET_DTYPE)
+        col = np.empty(m.nnz, dtype=INDEX_DTYPE)
+        val = np.empty(m.nnz, dtype=VALUE_DTYPE)
+        nnz = ctypes.c_int64()
+        _lib.check(lib.sellb_coo_to_crs(
+            _lib.ptr(m.rows), _lib.ptr(m.cols), _lib.ptr(m.vals), m.nnz, m.n_rows,
+            m.n_cols, _lib.ptr(rpt), _lib.ptr(col), _lib.ptr(val), ctypes.byref(nnz),
+            int(device), stream, 0))
+        n = nnz.value
+        return CRSMatrix(m.n_rows, m.n_cols, rpt, col[:n], val[:n])
     m = canonicalize_coo(m)
     rpt = np.zeros(m.n_rows + 1, dtype=OFFSET_DTYPE)
     np.cumsum(np.bincount(m.rows, minlength=m.n_rows), out=rpt[1:])
     return CRSMatrix(m.n_rows, m.n_cols, rpt, m.cols.astype(INDEX_DTYPE), m.vals)
+
+
+class DeviceCRS:
+    """Canonical CRS held in CUDA tensors (rpt int64, col int32, val f64) --
+    the device-side input of ``crs_to_sell_device``; ``to_host()`` gives the
+    CRSMatrix."""
+
+    def __init__(self, n_rows, n_cols, rpt, col, val):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.rpt, self.col, self.val = rpt, col, val
+
+    @property
+    def nnz(self):
+        return int(self.col.numel())
+
+    @property
+    def shape(self):
+        return (self.n_rows, self.n_cols)
+
+    def to_host(self):
+        return CRSMatrix(self.n_rows, self.n_cols, self.rpt.cpu().numpy(),
+                         self.col.cpu().numpy(), self.val.cpu().numpy())
+
+
+def coo_to_crs_device(m, *, device=0, stream=None):
+    """COO (a COOMatrix, or a tuple ``(n_rows, n_cols, rows, cols, vals)`` of
+    CUDA tensors int64/int64/f64) -> DeviceCRS, canonicalised on the GPU
+    (formats.py:89-108,169-175; bit-identical).  Runs on ``stream`` (default:
+    torch's current stream of ``device``)."""
+    import torch
+    lib = _lib.require_device()
+    dev = torch.device("cuda", device)
+    if isinstance(m, COOMatrix):
+        n_rows, n_cols = m.n_rows, m.n_cols
+        rows = torch.from_numpy(m.rows).to(dev)
+        cols = torch.from_numpy(m.cols).to(dev)
+        vals = torch.from_numpy(m.vals).to(dev)
+    else:
+        n_rows, n_cols, rows, cols, vals = m
+        _check_dims(n_rows, n_cols)
+        if not (rows.dtype == cols.dtype == torch.int64 and vals.dtype == torch.float64):
+            raise ParameterError("rows/cols must be int64 and vals float64 tensors")
+        if not rows.numel() == cols.numel() == vals.numel():
+            raise StructuralError("entry arrays must have equal length")
+        rows, cols, vals = rows.contiguous(), cols.contiguous(), vals.contiguous()
+    nnz_in = int(vals.numel())
+    rpt = torch.empty(int(n_rows) + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(nnz_in, dtype=torch.int32, device=dev)
+    val = torch.empty(nnz_in, dtype=torch.float64, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    nnz = ctypes.c_int64()
+    _lib.check(lib.sellb_coo_to_crs(
+        rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), nnz_in, int(n_rows), int(n_cols),
+        rpt.data_ptr(), col.data_ptr(), val.data_ptr(), ctypes.byref(nnz), int(device),
+        stream, 1))
+    n = nnz.value
+    return DeviceCRS(n_rows, n_cols, rpt, col[:n], val[:n])
+
+
+def coo_to_sell(m, C, sigma, align_bytes=1, permute_cols=False, *, device=0, stream=None):
+    """COO -> canonical CRS -> SELL-C-sigma without leaving the GPU: the
+    reference's ``crs_to_sell(coo_to_crs(m), ...)`` (formats.py:169-175,
+    295-393) in two device passes; identical SellMatrix."""
+    d = coo_to_crs_device(m, device=device, stream=stream)
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream(device).cuda_stream
+    return crs_to_sell_device(d.rpt, d.col, d.val, d.n_rows, d.n_cols, C, sigma,
+                              align_bytes, permute_cols, device=device, stream=stream)
 
 
 def crs_to_coo(m):

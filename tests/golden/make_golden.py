@@ -205,5 +205,62 @@ def make_cache_fixtures(out_dir):
                             built_row_lengths=s.row_lengths)
 
 
+def make_coo_fixtures(out_dir):
+    """COO -> CRS through the reference's coo_to_crs (formats.py:89-108,
+    169-175): unsorted input, duplicate runs of every length class NumPy's
+    pairwise summation distinguishes (< 8, 8..128, > 128), signed zeros,
+    canonical input (early return), empty rows, empty matrix."""
+    rng = np.random.default_rng(77)
+    cases = {}
+    # many short duplicate runs over a small grid
+    n = 4000
+    cases["dups_small"] = (50, 40, rng.integers(0, 50, n), rng.integers(0, 40, n),
+                           rng.standard_normal(n) * 10.0 ** rng.integers(-6, 6, n))
+    # long runs: one coordinate per run length
+    lens = [1, 2, 7, 8, 9, 15, 16, 17, 63, 64, 127, 128, 129, 130, 135, 136, 255, 256, 257,
+            300, 513, 1000, 2049]
+    r = np.concatenate([np.full(L, i % 7) for i, L in enumerate(lens)])
+    c = np.concatenate([np.full(L, 3 * i) for i, L in enumerate(lens)])
+    v = rng.standard_normal(len(r)) * 10.0 ** rng.integers(-9, 9, len(r))
+    p = rng.permutation(len(r))
+    cases["dups_long"] = (7, 3 * len(lens), r[p], c[p], v[p])
+    # signed zeros and exact cancellation
+    cases["zeros"] = (3, 3, [0, 0, 1, 1, 1, 2, 2], [0, 0, 1, 1, 1, 2, 2],
+                      [-0.0, -0.0, 0.0, -0.0, -0.0, 1.0, -1.0])
+    # canonical already: returned as is
+    m = random_coo(rng, 30, 30, 200, allow_zero_values=True)
+    cases["canonical"] = (30, 30, m.rows, m.cols, m.vals)
+    # unsorted, no duplicates, empty leading/trailing/middle rows
+    rows = np.array([9, 3, 3, 5, 9, 3], np.int64)
+    cols = np.array([0, 4, 1, 2, 7, 0], np.int64)
+    cases["empty_rows"] = (12, 8, rows, cols, rng.standard_normal(6))
+    cases["empty"] = (5, 4, np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    cases["no_rows"] = (0, 0, np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    # a bigger mixed case
+    n = 30000
+    cases["mixed"] = (3000, 2500, rng.integers(0, 3000, n), rng.integers(0, 2500, n) // 7,
+                      rng.uniform(-1, 1, n))
+    for name, (nr, nc, rows, cols, vals) in cases.items():
+        coo = COOMatrix(nr, nc, np.asarray(rows), np.asarray(cols), np.asarray(vals, float))
+        crs = coo_to_crs(coo)
+        np.savez_compressed(os.path.join(out_dir, f"coo_{name}.npz"), n_rows=nr, n_cols=nc,
+                            rows=coo.rows, cols=coo.cols, vals=coo.vals, rpt=crs.rpt,
+                            col=crs.col, val=crs.val)
+    # out-of-bounds messages (formats.py:58-70)
+    errs = []
+    for nr, nc, rows, cols in ((4, 4, [0, 5, -1], [0, 0, 0]), (4, 4, [0, 1], [3, 9]),
+                               (4, 4, [2, 7], [9, 0])):
+        try:
+            COOMatrix(nr, nc, rows, cols, np.ones(len(rows)))
+            errs.append("")
+        except sellkit.StructuralError as e:
+            errs.append(str(e))
+    np.savez_compressed(os.path.join(out_dir, "coo_errors.npz"), messages=np.array(errs))
+
+
 if __name__ == "__main__":
-    main()
+    if "--coo-only" in sys.argv:
+        make_coo_fixtures(HERE)
+    else:
+        main()
+        make_coo_fixtures(HERE)
