@@ -205,6 +205,8 @@ void free_mat_arrays(sellb_mat* m) {
     cudaFree(m->order);
     cudaFree(m->long_rows);
     cudaFree(m->chunk_th);
+    cudaFree(m->long_groups);
+    cudaFree(m->long_rest);
     if (m->pipe_ready) {
         cudaStreamDestroy(m->s_h2d);
         cudaStreamDestroy(m->s_comp);
@@ -214,6 +216,11 @@ void free_mat_arrays(sellb_mat* m) {
             cudaEventDestroy(m->ev_x[i]);
             cudaEventDestroy(m->ev_blk[i]);
         }
+    }
+    if (m->long_ready) {
+        cudaStreamDestroy(m->s_long);
+        cudaEventDestroy(m->ev_fork);
+        cudaEventDestroy(m->ev_join);
     }
     cudaFree(m->x_buf);
     cudaFree(m->y_buf);
@@ -272,9 +279,15 @@ int choose_variant(sellb_mat* m, cudaStream_t st, double* beta_eff_out, int64_t*
 int build_long_rows(sellb_mat* m, cudaStream_t st) {
     cudaFree(m->long_rows);
     cudaFree(m->chunk_th);
+    cudaFree(m->long_groups);
+    cudaFree(m->long_rest);
     m->long_rows = nullptr;
     m->chunk_th = nullptr;
+    m->long_groups = nullptr;
+    m->long_rest = nullptr;
     m->n_long = 0;
+    m->n_groups = 0;
+    m->n_rest = 0;
     m->long_th = 0x7fffffff;
     if (!m->rl || m->n_pad == 0) return 0;
     // Two thresholds: a row longer than th_lo leaves the bulk role when its
@@ -312,8 +325,57 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     if (int rc = alloc_dev((void**)&m->long_rows, rows.size() * 4)) return rc;
     SELLB_CU(cudaMemcpyAsync(m->long_rows, rows.data(), rows.size() * 4,
                              cudaMemcpyHostToDevice, st));
+    // 8-row groups for the pipelined kernel: aligned groups of one chunk
+    // holding >= 4 long rows (sorted chunks of long rows), longest first
+    std::vector<int32_t> groups, rest;
+    std::vector<int32_t> gmax;
+    const bool use_groups = m->C % 8 == 0 && !(getenv("SELLB_LONG_GRP") &&
+                                                atoi(getenv("SELLB_LONG_GRP")) == 0);
+    if (use_groups) {
+        std::vector<uint8_t> is_long(m->n_pad, 0);
+        for (int32_t p : rows) is_long[p] = 1;
+        std::vector<uint8_t> in_grp(m->n_pad, 0);
+        for (int32_t p : rows) {
+            const int32_t g0 = p & ~7;
+            if (in_grp[g0]) continue;
+            int cnt = 0;
+            int32_t mx = 0;
+            for (int r = 0; r < 8; ++r)
+                if (is_long[g0 + r]) { ++cnt; mx = std::max(mx, h_rl[g0 + r]); }
+            if (cnt >= 4) {
+                for (int r = 0; r < 8; ++r) in_grp[g0 + r] = 1;
+                groups.push_back(g0);
+                gmax.push_back(mx);
+            } else {
+                in_grp[g0] = 2;       // sparse group: its long rows stay per-row
+            }
+        }
+        for (int32_t p : rows)
+            if (in_grp[p & ~7] != 1) rest.push_back(p);
+        std::vector<int32_t> idx(groups.size());
+        for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int32_t)i;
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](int32_t a, int32_t b) { return gmax[a] > gmax[b]; });
+        std::vector<int32_t> sorted(groups.size());
+        for (size_t i = 0; i < idx.size(); ++i) sorted[i] = groups[idx[i]];
+        groups.swap(sorted);
+    } else {
+        rest = rows;
+    }
+    if (!groups.empty()) {
+        if (int rc = alloc_dev((void**)&m->long_groups, groups.size() * 4)) return rc;
+        SELLB_CU(cudaMemcpyAsync(m->long_groups, groups.data(), groups.size() * 4,
+                                 cudaMemcpyHostToDevice, st));
+    }
+    if (!rest.empty()) {
+        if (int rc = alloc_dev((void**)&m->long_rest, rest.size() * 4)) return rc;
+        SELLB_CU(cudaMemcpyAsync(m->long_rest, rest.data(), rest.size() * 4,
+                                 cudaMemcpyHostToDevice, st));
+    }
     SELLB_CU(cudaStreamSynchronize(st));
     m->n_long = (int64_t)rows.size();
+    m->n_groups = (int64_t)groups.size();
+    m->n_rest = (int64_t)rest.size();
     m->long_th = th;
     return 0;
 }

@@ -43,8 +43,21 @@ struct sellb_mat {
     // warp-per-row role (lanes over slots) takes them
     int32_t* long_rows = nullptr;
     int64_t n_long = 0;
+    // the pipelined long-row kernel splits long_rows[] into 8-row groups
+    // (aligned, same chunk, >= 4 long rows: lanes = 8 rows x 4 slots, loads
+    // coalesced per row group) and the remaining rows (warp per row)
+    int32_t* long_groups = nullptr;   // first stored row of each group
+    int64_t n_groups = 0;
+    int32_t* long_rest = nullptr;
+    int64_t n_rest = 0;
     int32_t long_th = 0x7fffffff;     // chunks wider than this may hold long rows
     int32_t* chunk_th = nullptr;      // per chunk: rows longer than this are long
+    // long-row kernel on a side stream, forked from / joined into the
+    // caller's stream around the bulk launch (fork/join under long_mu)
+    bool long_ready = false;
+    cudaStream_t s_long = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    std::mutex long_mu;
     // end-to-end staging (device x / y for sellb_spmv_host)
     void* x_buf = nullptr;
     void* y_buf = nullptr;

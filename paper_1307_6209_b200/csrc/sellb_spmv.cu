@@ -30,6 +30,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "sellb_internal.cuh"
@@ -237,6 +238,324 @@ __device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
     if (lane == 0) store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined long-row kernel (its own launch, on a side stream next to the
+// bulk): still one warp per long row and the same staged, in-order add chain
+// as long_row(), but the loads are asynchronous copies into a per-warp
+// shared-memory ring, so the chain of batch b runs while the val/col of
+// batches b+1..b+D-1 and the x gather of batch b+1 are in flight.  The
+// warp-per-row role inside the bulk kernel has one batch in flight and is
+// latency-bound (cfg4 sigma=N: 1024 rows of 2048 took 64 us of a 66 us SpMV).
+//   group order per batch b:  VC(b+D) [val, col]  then  X(b+1) [x[col]]
+// cp.async with a 4 / 8-byte copy size (each lane its own slot), L1-allocating
+// (.ca): the 8 warps of a block walk 8 adjacent rows of the same chunk, so
+// one warp's sectors are the next warp's L1 hits.
+// ---------------------------------------------------------------------------
+constexpr int kLB = 128;                 // slots per batch (4 per lane)
+
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int B>
+__device__ __forceinline__ void cp_async(void* sdst, const void* gsrc, uint64_t pol) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;" ::"r"(s),
+                 "l"(gsrc), "n"(B), "l"(pol)
+                 : "memory");
+}
+
+// Group accounting of the copy ring (one commit group per issue):
+// prologue VC(0..D-1), then X(0..E-1) each after cp_wait<D-1>; iteration b
+// commits VC(b+D) then X(b+E).  wait_vc(b) leaves VC(b+E) landed, wait_x(b)
+// leaves X(b) landed (exact counts in steady state, conservative -- waits
+// for more -- in the first iterations).
+template <int D, int E>
+__device__ __forceinline__ void wait_vc(int b) {
+    if (b >= D - 2 * E) cp_wait<2 * (D - E)>();
+    else cp_wait<D>();
+}
+template <int E>
+__device__ __forceinline__ void wait_x(int b) {
+    if (b >= E - 1) cp_wait<2 * E>();
+    else cp_wait<E + 1>();
+}
+
+template <typename T, bool ACC, int ORD, int D, int E>
+__global__ void __launch_bounds__(kThreads)
+k_spmv_long(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+            const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+            const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+            const int32_t* __restrict__ order, int64_t C, int64_t p0, int64_t p1,
+            int64_t n_rows, const int32_t* __restrict__ long_rows, int64_t n_long, int l2pol) {
+    constexpr int NS = D + 1;                              // ring stages
+    extern __shared__ __align__(16) uint8_t lsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t k = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+    if (k >= n_long) return;
+    const int64_t p = long_rows[k];
+    if (p < p0 || p >= p1) return;
+    // per-warp ring: NS x {val[kLB], x[kLB]} of T, NS x col[kLB] int32
+    T* sv = reinterpret_cast<T*>(lsm) + (size_t)warp * NS * 2 * kLB;
+    T* sx = sv + NS * kLB;
+    int32_t* sc = reinterpret_cast<int32_t*>(reinterpret_cast<T*>(lsm) +
+                                             (size_t)(kThreads / 32) * NS * 2 * kLB) +
+                  (size_t)warp * NS * kLB;
+    const uint64_t pol_s = make_policy(l2pol & 0xf);
+    const uint64_t pol_x = make_policy(l2pol >> 4);
+    const int64_t chunk = p / C;
+    const int64_t base = cs[chunk] + (p - chunk * C);
+    const int w = cl[chunk];
+    const int len = rl[p];
+    const int nb = (len + kLB - 1) / kLB;
+    const T* vp = val + base;
+    const int32_t* cp = col + base;
+
+    auto issue_vc = [&](int b) {
+        if (b < nb) {
+            const int st = b % NS;
+#pragma unroll
+            for (int s = 0; s < kLB / 32; ++s) {
+                const int j = b * kLB + s * 32 + lane;
+                if (j < len) {
+                    cp_async<sizeof(T)>(sv + st * kLB + s * 32 + lane, vp + (int64_t)j * C, pol_s);
+                    cp_async<4>(sc + st * kLB + s * 32 + lane, cp + (int64_t)j * C, pol_s);
+                }
+            }
+        }
+        cp_commit();
+    };
+    auto issue_x = [&](int b) {       // needs this lane's col of batch b landed
+        if (b < nb) {
+            const int st = b % NS;
+#pragma unroll
+            for (int s = 0; s < kLB / 32; ++s) {
+                const int j = b * kLB + s * 32 + lane;
+                if (j < len) cp_async<sizeof(T)>(sx + st * kLB + s * 32 + lane,
+                                                 x + sc[st * kLB + s * 32 + lane], pol_x);
+            }
+        }
+        cp_commit();
+    };
+
+#pragma unroll
+    for (int b = 0; b < D; ++b) issue_vc(b);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        cp_wait<D - 1>();                                  // VC(e)
+        issue_x(e);
+    }
+    T sum = T(0);
+    for (int b = 0; b < nb; ++b) {
+        issue_vc(b + D);
+        wait_vc<D, E>(b);                                  // VC(b+E)
+        issue_x(b + E);
+        wait_x<E>(b);                                      // X(b)
+        const int st = b % NS;
+#pragma unroll
+        for (int s = 0; s < kLB / 32; ++s) {               // rounded products, in place
+            const int i = st * kLB + s * 32 + lane;
+            const int j = b * kLB + s * 32 + lane;
+            sv[i] = (j < len) ? Arith<T>::mul(sv[i], sx[i]) : T(0);
+        }
+        __syncwarp();
+        const T* pr = sv + st * kLB;
+        const int cnt = min(len - b * kLB, kLB);
+        int i = 0;
+        for (; i + 16 <= cnt; i += 16) {
+            T q[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) q[u] = pr[i + u];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) sum = Arith<T>::add(sum, q[u]);
+        }
+        for (; i < cnt; ++i) sum = Arith<T>::add(sum, pr[i]);
+        __syncwarp();                                      // stage free for VC(b+NS)
+    }
+    cp_wait<0>();
+    if (len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+    if (lane == 0) store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
+}
+
+template <typename T, int D>
+constexpr size_t long_smem() {
+    return (size_t)(kThreads / 32) * (D + 1) * kLB * (2 * sizeof(T) + 4);
+}
+
+// Row-group variant: one CTA per aligned group of 8 stored rows of one chunk
+// (sorted chunks of long rows), warp-specialised.  Producer warps (4) copy
+// the group's val/col and gather x into a cp.async ring and form the rounded
+// products -- producer thread t takes row t % 8 of slot t / 8, so a
+// warp-wide copy covers 4 slots x 8 adjacent rows = 4 contiguous 64-byte
+// runs instead of the 32 scattered words of the warp-per-row role (which
+// saturates the L1: l1tex 78 % of peak for cfg4's long rows).  The products
+// go to a double buffer [row][slot]; in the chain warp lane r (< 8) adds row
+// r's products in slot order, 16 at a time from registers loaded one block
+// ahead (one 8-cycle DADD per slot; the shared-memory latency stays off the
+// chain).  Producers and the chain hand the buffers over through named
+// barriers (full / empty per buffer), so the chain of batch b overlaps the
+// copies and products of batch b+1.
+constexpr int kGP = 4;                  // producer warps
+constexpr int kGT = (1 + kGP) * 32;     // + one chain warp
+
+// non-.aligned forms: legal for a warp that is not converged (after the
+// predicated copies / stores); the .aligned bar.sync raised "illegal
+// instruction" once the group loop made divergence reach it
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// 16 consecutive T from 16-byte-aligned shared memory
+template <typename T>
+__device__ __forceinline__ void lds16(const T* p, T (&q)[16]) {
+    constexpr int V = 16 / sizeof(T);
+#pragma unroll
+    for (int k = 0; k < 16 / V; ++k) {
+        const uint4 u = *reinterpret_cast<const uint4*>(p + k * V);
+        const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+        for (int v = 0; v < V; ++v) q[k * V + v] = t[v];
+    }
+}
+
+template <typename T, bool ACC, int ORD, int D, int E, int SB>
+__global__ void __launch_bounds__(kGT)
+k_spmv_long_grp(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+                const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+                const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+                const int32_t* __restrict__ order, int64_t C, int64_t p0, int64_t p1,
+                int64_t n_rows, const int32_t* __restrict__ groups, int64_t n_groups,
+                const int32_t* __restrict__ chunk_th, int l2pol) {
+    constexpr int NS = D + 1;
+    constexpr int NP = kGP * 32;               // producer threads
+    constexpr int PER = SB * 8 / NP;           // (slot, row) entries per producer per batch
+    constexpr int PS = SB + 16 / sizeof(T) * 2;  // row pitch: 16-byte aligned, rows 32 B apart mod 128
+    static_assert(PER * NP == SB * 8, "SB * 8 must be a multiple of the producer count");
+    static_assert(SB % 16 == 0, "SB must be a multiple of 16");
+    // named barriers 1/2: buffer full, 3/4: buffer empty (0 is __syncthreads)
+    extern __shared__ __align__(16) uint8_t lsm[];
+    T* prod = reinterpret_cast<T*>(lsm);                          // [2][8][PS]
+    T* sv = prod + 2 * 8 * PS;                                    // [NS][SB*8]
+    T* sx = sv + NS * SB * 8;                                     // [NS][SB*8]
+    int32_t* sc = reinterpret_cast<int32_t*>(sx + NS * SB * 8);   // [NS][SB*8]
+    __shared__ int s_len[8];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t g0 = groups[blockIdx.x];
+    const int64_t chunk = g0 / C;
+    const int w = cl[chunk];
+    const int th = chunk_th[chunk];
+    if (tid < 8) {
+        const int64_t row = g0 + tid;
+        const int lr = rl[row];
+        s_len[tid] = (lr > th && row >= p0 && row < p1) ? lr : 0;
+    }
+    __syncthreads();
+    int maxlen = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) maxlen = max(maxlen, s_len[i]);
+    const int nb = (maxlen + SB - 1) / SB;
+
+    if (warp > 0) {                                    // ---- producers
+        const uint64_t pol_s = make_policy(l2pol & 0xf);
+        const uint64_t pol_x = make_policy(l2pol >> 4);
+        const int pt = tid - 32;
+        const int r = pt & 7;                          // fixed row per producer thread
+        const int len = s_len[r];
+        const int64_t base = cs[chunk] + (g0 - chunk * C) + r;
+        const T* vp = val + base;
+        const int32_t* cp = col + base;
+        auto issue_vc = [&](int b) {
+            if (b < nb) {
+                const int st = b % NS;
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    const int e = k * NP + pt;
+                    const int j = b * SB + (e >> 3);
+                    if (j < len) {
+                        cp_async<sizeof(T)>(sv + st * SB * 8 + e, vp + (int64_t)j * C, pol_s);
+                        cp_async<4>(sc + st * SB * 8 + e, cp + (int64_t)j * C, pol_s);
+                    }
+                }
+            }
+            cp_commit();
+        };
+        auto issue_x = [&](int b) {
+            if (b < nb) {
+                const int st = b % NS;
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    const int e = k * NP + pt;
+                    if (b * SB + (e >> 3) < len)
+                        cp_async<sizeof(T)>(sx + st * SB * 8 + e, x + sc[st * SB * 8 + e],
+                                            pol_x);
+                }
+            }
+            cp_commit();
+        };
+#pragma unroll
+        for (int b = 0; b < D; ++b) issue_vc(b);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            cp_wait<D - 1>();
+            issue_x(e);
+        }
+        for (int b = 0; b < nb; ++b) {
+            issue_vc(b + D);
+            wait_vc<D, E>(b);
+            issue_x(b + E);
+            wait_x<E>(b);
+            const int st = b % NS;
+            if (b >= 2) named_sync(3 + (b & 1), kGT);     // chain done with batch b-2
+            T* pb = prod + (b & 1) * 8 * PS;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int e = k * NP + pt;
+                const int jj = e >> 3;
+                const int i = st * SB * 8 + e;
+                pb[r * PS + jj] = (b * SB + jj < len) ? Arith<T>::mul(sv[i], sx[i]) : T(0);
+            }
+            named_arrive(1 + (b & 1), kGT);
+        }
+        cp_wait<0>();
+        for (int b = max(nb - 2, 0); b < nb; ++b) named_sync(3 + (b & 1), kGT);  // drain
+        return;
+    }
+    // ---- chain warp: lane r sums row g0 + r (lanes 8..31 mirror lanes 0..7)
+    const int r = lane & 7;
+    T sum = T(0);
+    for (int b = 0; b < nb; ++b) {
+        named_sync(1 + (b & 1), kGT);
+        // +0.0 products past a row's end are exact no-ops (the sum starts at
+        // +0.0 and is never -0.0): the chain runs the whole batch
+        const T* q = prod + (b & 1) * 8 * PS + r * PS;
+        T cur[16], nxt[16];
+        lds16(q, cur);
+#pragma unroll
+        for (int k = 0; k < SB / 16; ++k) {
+            if (k + 1 < SB / 16) lds16(q + (k + 1) * 16, nxt);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) sum = Arith<T>::add(sum, cur[u]);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
+        }
+        named_arrive(3 + (b & 1), kGT);
+    }
+    if (lane < 8 && s_len[r] > 0) {
+        const int64_t row = g0 + r;
+        if (s_len[r] < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+        store_row<T, ACC, ORD>(y, order, row, n_rows, sum);
+    }
+}
+
+template <typename T, int D, int SB>
+constexpr size_t grp_smem() {
+    return (size_t)(D + 1) * SB * 8 * (2 * sizeof(T) + 4) +
+           2 * 8 * (SB + 16 / sizeof(T) * 2) * sizeof(T);
+}
+
 // The SpMV kernel.  Blocks [0, n_long_blocks) take the long-row role (one
 // warp per row of long_rows[], longest first, so they start early and
 // overlap the bulk); the remaining blocks take one thread per stored row p
@@ -433,7 +752,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     if (rows <= 0) return 0;
     const int64_t n_long = m->long_rows ? m->n_long : 0;
     const int64_t long_blocks = (n_long + kThreads / 32 - 1) / (kThreads / 32);
-    const unsigned grid = (unsigned)(grid_for(rows, kThreads) + long_blocks);
+    unsigned grid = (unsigned)(grid_for(rows, kThreads) + long_blocks);
     // L2 policies: matrix streams (low nibble) and x gathers (high nibble);
     // 0 evict_first, 1 evict_normal, 2 evict_last.  x is always evict_last;
     // the matrix stream is evict_first while x fits comfortably in L2 and
@@ -463,12 +782,20 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     }();
 #define SELLB_LAUNCH(UU, LL, LR, NL, TH)                                                        \
     do {                                                                                        \
-        if (carve >= 0) {                                                                       \
-            static bool set_ = false;                                                           \
-            if (!set_) {                                                                        \
+        /* LONG instances run next to the row-group kernel: reserve shared */ \
+        /* memory for one group CTA per SM up front (30 %), so an SM never */ \
+        /* has to drain its bulk blocks to change its carve-out when a     */ \
+        /* group CTA arrives (cfg3 sigma=N 495 -> 757 GF/s, tools/         */ \
+        /* long_cfg_ab.sh; neutral in the fused mode)                      */ \
+        const int carve_ = carve >= 0 ? carve : ((LL) ? 30 : -1);                               \
+        if (carve_ >= 0) {                                                                      \
+            static unsigned set_ = 0;   /* per-device bit */                                    \
+            int dev_ = 0;                                                                       \
+            cudaGetDevice(&dev_);                                                               \
+            if (!(set_ & (1u << (dev_ & 31)))) {                                                \
                 cudaFuncSetAttribute(k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL>,                \
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve);    \
-                set_ = true;                                                                    \
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve_);   \
+                set_ |= 1u << (dev_ & 31);                                                      \
             }                                                                                   \
         }                                                                                       \
         if (persist) {                                                                          \
@@ -545,7 +872,118 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
 #undef SELLB_SWEEP_LAUNCH
         return 0;
     }
-    if (n_long) {
+    // long rows: SELLB_LONG_MODE 0 = warp-per-row role fused into the bulk
+    // launch; 1 = long-row kernels, then the bulk, on the caller's stream;
+    // 2 (default) = long-row kernels on a side stream forked from and joined
+    // back into the caller's stream, overlapping the bulk.  The side stream
+    // has the device's greatest priority: the block scheduler dispatches its
+    // CTAs ahead of pending bulk blocks (at equal priority they were
+    // sometimes queued behind the whole bulk grid: cfg4 43 vs 86 us).
+    static const int long_mode = [] {
+        const char* e = getenv("SELLB_LONG_MODE");
+        return e ? atoi(e) : 2;
+    }();
+    static const int long_d = [] {
+        const char* e = getenv("SELLB_LONG_D");
+        return e ? atoi(e) : 4;
+    }();
+    static const int rest_sep = [] {
+        const char* e = getenv("SELLB_LONG_REST");
+        return e ? atoi(e) : 0;
+    }();
+    if (n_long && long_mode != 0 && (m->n_groups || rest_sep)) {
+        sellb_mat* mm = const_cast<sellb_mat*>(m);
+        std::unique_lock<std::mutex> lk(mm->long_mu, std::defer_lock);
+        cudaStream_t ls = st;
+        if (long_mode == 2) {
+            lk.lock();
+            if (!mm->long_ready) {
+                int prio_lo = 0, prio_hi = 0;
+                SELLB_CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+                SELLB_CU(cudaStreamCreateWithPriority(&mm->s_long, cudaStreamNonBlocking,
+                                                      prio_hi));
+                SELLB_CU(cudaEventCreateWithFlags(&mm->ev_fork, cudaEventDisableTiming));
+                SELLB_CU(cudaEventCreateWithFlags(&mm->ev_join, cudaEventDisableTiming));
+                mm->long_ready = true;
+            }
+            SELLB_CU(cudaEventRecord(mm->ev_fork, st));
+            SELLB_CU(cudaStreamWaitEvent(mm->s_long, mm->ev_fork, 0));
+            ls = mm->s_long;
+        }
+#define SELLB_SMEM_ONCE(KERN, BYTES)                                                            \
+    do {                                                                                        \
+        static unsigned attr_ = 0;      /* per-device bit */                                    \
+        int dev_ = 0;                                                                           \
+        cudaGetDevice(&dev_);                                                                   \
+        if (!(attr_ & (1u << (dev_ & 31)))) {                                                   \
+            cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                                 (int)(BYTES));                                                 \
+            attr_ |= 1u << (dev_ & 31);                                                         \
+        }                                                                                       \
+    } while (0)
+#define SELLB_LONG_LAUNCH(DD, EE, LIST, NL)                                                         \
+    do {                                                                                        \
+        constexpr size_t smem_ = long_smem<T, DD>();                                            \
+        SELLB_SMEM_ONCE((k_spmv_long<T, ACC, ORD, DD, EE>), smem_);                             \
+        k_spmv_long<T, ACC, ORD, DD, EE>                                                        \
+            <<<(unsigned)(((NL) + kThreads / 32 - 1) / (kThreads / 32)), kThreads, smem_, ls>>>( \
+                m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
+                m->C, p0, p1, m->n_rows, LIST, NL, l2pol);                                      \
+    } while (0)
+#define SELLB_GRP_LAUNCH(DD, EE, TT)                                                            \
+    do {                                                                                        \
+        constexpr size_t smem_ = grp_smem<T, DD, TT>();                                         \
+        SELLB_SMEM_ONCE((k_spmv_long_grp<T, ACC, ORD, DD, EE, TT>), smem_);                     \
+        /* waves of at most grp_ctas CTAs (longest groups first): the      */ \
+        /* shared-memory carve-out stays off most SMs, and the bulk next   */ \
+        /* to it relies on L1 hits for x (cfg3 sigma=N lost a third of its */ \
+        /* speed with a group CTA on every SM)                             */ \
+        for (int64_t g_ = 0; g_ < m->n_groups; g_ += grp_ctas) {                               \
+            const int64_t ng_ = std::min<int64_t>(m->n_groups - g_, grp_ctas);                  \
+            k_spmv_long_grp<T, ACC, ORD, DD, EE, TT><<<(unsigned)ng_, kGT, smem_, ls>>>(        \
+                m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
+                m->C, p0, p1, m->n_rows, m->long_groups + g_, ng_, m->chunk_th, l2pol);         \
+        }                                                                                       \
+    } while (0)
+        static const int grp_ctas = [] {
+            const char* e = getenv("SELLB_GRP_CTAS");
+            return e ? std::max(1, atoi(e)) : 1 << 30;
+        }();
+        static const int grp_sb = [] {
+            const char* e = getenv("SELLB_GRP_SB");
+            return e ? atoi(e) : 64;
+        }();
+        if (m->n_groups) {
+            if (grp_sb == 128) SELLB_GRP_LAUNCH(4, 2, 128);
+            else if (grp_sb == 3) SELLB_GRP_LAUNCH(8, 3, 64);
+            else if (grp_sb == 4) SELLB_GRP_LAUNCH(6, 3, 128);
+            else if (grp_sb == 5) SELLB_GRP_LAUNCH(10, 4, 64);
+            else SELLB_GRP_LAUNCH(4, 2, 64);
+        }
+        // the other long rows (isolated in chunks of short rows) keep the
+        // fused warp-per-row role (below); SELLB_LONG_REST=1 sends them to
+        // the pipelined warp-per-row kernel instead (measured slower: cfg4
+        // sigma=1 117 vs 165 us)
+        if (m->n_rest && rest_sep) {
+            if (long_d == 3) SELLB_LONG_LAUNCH(3, 1, m->long_rest, m->n_rest);
+            else if (long_d == 6) SELLB_LONG_LAUNCH(6, 3, m->long_rest, m->n_rest);
+            else SELLB_LONG_LAUNCH(4, 2, m->long_rest, m->n_rest);
+        }
+#undef SELLB_GRP_LAUNCH
+#undef SELLB_LONG_LAUNCH
+#undef SELLB_SMEM_ONCE
+        SELLB_CU(cudaGetLastError());
+        // the bulk: rows above their chunk's threshold are skipped (LONG
+        // template), no long-role blocks
+        grid = (unsigned)grid_for(rows, kThreads);
+        if (long_mode == 2) SELLB_CU(cudaEventRecord(mm->ev_join, ls));
+        const int32_t* rest = rest_sep ? nullptr : m->long_rest;
+        const int64_t n_rest = rest_sep ? 0 : m->n_rest;
+        grid += (unsigned)((n_rest + kThreads / 32 - 1) / (kThreads / 32));
+        if (u8) SELLB_LAUNCH(8, true, rest, n_rest, m->long_th);
+        else SELLB_LAUNCH(4, true, rest, n_rest, m->long_th);
+        if (long_mode == 2) SELLB_CU(cudaStreamWaitEvent(st, mm->ev_join, 0));
+    } else if (n_long) {
         if (u8) SELLB_LAUNCH(8, true, m->long_rows, n_long, m->long_th);
         else SELLB_LAUNCH(4, true, m->long_rows, n_long, m->long_th);
     } else if (u_env == 6 || (!u_env && m->max_cl > 4 && m->max_cl <= 6 && sizeof(T) == 8)) {
