@@ -549,8 +549,9 @@ def run_ours(args):
         "config": {"workload": f"{desc}, SELL-{args.C}-{sigma}", "C": args.C, "sigma": sigma,
                    "n_rows": n_rows, "nnz": nnz, "slots": slots,
                    "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
-                   "l2": ("flushed between steps (%d MB scratch write); value from the "
-                          "SpMV's own events" % (4 * l2_bytes // 2**20)) if flush is not None
+                   "l2": ("flushed between steps (%d MB scratch write, then half of it "
+                          "read back so the L2 holds clean lines); value from the SpMV's "
+                          "own events" % (4 * l2_bytes // 2**20)) if flush is not None
                    else "inputs larger than L2 (V_alg %.0f MB > %d MB L2)" % (
                        v_alg / 1e6, l2_bytes // 2**20),
                    "build_s": round(build_s, 4), "build": wl.get("build"),
@@ -568,7 +569,7 @@ def run_ours(args):
                 "matches_device": e2e_ok},
         "cpu_baseline": cpu,
         "clocks": clk,
-        "gpu_launches": args.steps * (2 if flush is not None else 1),
+        "gpu_launches": args.steps * (3 if flush is not None else 1),
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -182,7 +182,9 @@ int sellb_sector_occupancy(const sellb_mat* m, double* beta_eff, int64_t* val_se
 /* Device read-reduce / copy bandwidth kernels (membench.py:52-116 analogs). */
 int sellb_read_sum(const double* a_dev, int64_t n, double* out_host, void* stream);
 int sellb_copy(const double* src_dev, double* dst_dev, int64_t n, void* stream);
-/* Overwrite a scratch buffer larger than L2 (timing hygiene). */
+/* Overwrite a scratch buffer larger than L2, then read half of it back so the
+ * L2 holds clean lines (timing hygiene: the next kernel neither hits its own
+ * data nor pays for the flush's write-backs). */
 int sellb_l2_flush(void* scratch_dev, int64_t bytes, void* stream);
 
 /* Padding fix-up of the row-partitioned path: the reference adds 0*x[0]
