@@ -42,6 +42,7 @@ extern "C" {
 #define SELLB_EDIM       -2   /* DimensionError   */
 #define SELLB_ESTRUCT    -3   /* StructuralError  */
 #define SELLB_ERESOURCE  -4   /* ResourceError: no device, CUDA error, OOM, NCCL */
+#define SELLB_EFORMAT    -5   /* FormatError: text outside the fast parser's grammar */
 
 /* value types */
 #define SELLB_F64 0
@@ -229,6 +230,20 @@ int sellb_gen_hamiltonian_fill(int64_t n, int64_t r0, int64_t r1, const int64_t*
 int sellb_coo_to_crs(const int64_t* rows, const int64_t* cols, const double* vals, int64_t nnz,
                      int64_t n_rows, int64_t n_cols, int64_t* rpt, int32_t* col, double* val,
                      int64_t* nnz_out, int32_t device, void* stream, int32_t ptrs_on_device);
+
+/* Matrix Market body (host, multi-threaded; io.py:125-162 / 252-259).
+ * parse: the text after the size line -> out[n_entries * width] (row-major,
+ * like np.loadtxt(..., comments="%")); capacity max_entries rows.  Returns
+ * SELLB_EFORMAT for anything outside plain decimal / inf / nan tokens with
+ * exactly `width` tokens per data line, or more than max_entries rows: the
+ * caller then re-parses with the reference-compatible path for the exact
+ * FormatError.  n_threads <= 0: all hardware threads.
+ * format: "%d %d %.17g\n" lines of (rows+1, cols+1, vals) as np.savetxt
+ * writes them; cap >= 64 * n suffices. */
+int sellb_mm_parse_body(const char* text, int64_t len, int32_t width, int64_t max_entries,
+                        double* out, int64_t* n_entries, int32_t n_threads);
+int sellb_mm_format_body(const int64_t* rows, const int64_t* cols, const double* vals,
+                         int64_t n, char* out, int64_t cap, int64_t* used, int32_t n_threads);
 
 /* Pinned host buffers for the end-to-end path. */
 int sellb_host_alloc(size_t bytes, void** out);

@@ -9,7 +9,7 @@ import ctypes
 import os
 import threading
 
-from .errors import (DimensionError, ParameterError, ResourceError,
+from .errors import (DimensionError, FormatError, ParameterError, ResourceError,
                      StructuralError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -34,7 +34,7 @@ EXPORTED = (
     "sellb_host_alloc", "sellb_host_free", "sellb_gather", "sellb_scatter",
     "sellb_pad_fixup", "sellb_gen_hamiltonian_rpt", "sellb_gen_hamiltonian_fill",
     "sellb_export_range", "sellb_infer_row_lengths", "sellb_chunk_flags",
-    "sellb_coo_to_crs",
+    "sellb_coo_to_crs", "sellb_mm_parse_body", "sellb_mm_format_body",
 )
 
 
@@ -104,6 +104,10 @@ _PROTOS = {
     "sellb_chunk_flags": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "sellb_coo_to_crs": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
                                         ctypes.POINTER(_i64), _i32, _vp, _i32]),
+    "sellb_mm_parse_body": (ctypes.c_int, [_vp, _i64, _i32, _i64, _vp, ctypes.POINTER(_i64),
+                                           _i32]),
+    "sellb_mm_format_body": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64,
+                                            ctypes.POINTER(_i64), _i32]),
 }
 
 _lib = None
@@ -161,7 +165,7 @@ def last_error():
 
 
 _ERRORS = {-1: ParameterError, -2: DimensionError, -3: StructuralError,
-           -4: ResourceError}
+           -4: ResourceError, -5: FormatError}
 
 
 def check(rc):

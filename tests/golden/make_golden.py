@@ -18,6 +18,7 @@ import os
 import sys
 import importlib.util
 import glob
+import gzip
 
 import numpy as np
 
@@ -258,9 +259,127 @@ def make_coo_fixtures(out_dir):
     np.savez_compressed(os.path.join(out_dir, "coo_errors.npz"), messages=np.array(errs))
 
 
+MM_TEXTS = {
+    "general": "%%MatrixMarket matrix coordinate real general\n% a comment\n3 4 3\n"
+               "1 1 2.5\n2 3 -1e-3\n3 4 7\n",
+    "integer": "%%MatrixMarket matrix coordinate integer general\n2 2 2\n1 1 3\n2 2 -4\n",
+    "pattern": "%%MatrixMarket matrix coordinate pattern general\n2 2 2\n1 2\n2 1\n",
+    "symmetric": "%%MatrixMarket matrix coordinate real symmetric\n3 3 3\n1 1 5\n2 1 2\n"
+                 "3 3 1\n",
+    "skew": "%%MatrixMarket matrix coordinate real skew-symmetric\n3 3 2\n2 1 4\n3 2 -1.5\n",
+    "skew_diag": "%%MatrixMarket matrix coordinate real skew-symmetric\n2 2 2\n2 1 1\n"
+                 "2 2 3\n",
+    "duplicates": "%%MatrixMarket matrix coordinate real general\n2 2 4\n1 1 1.5\n2 2 1\n"
+                  "1 1 2.25\n1 1 -0.75\n",
+    "array_general": "%%MatrixMarket matrix array real general\n2 3\n1\n2\n0\n4\n5\n0\n",
+    "array_symmetric": "%%MatrixMarket matrix array real symmetric\n3 3\n1\n2\n3\n4\n"
+                       "0\n6\n",
+    "array_skew": "%%MatrixMarket matrix array real skew-symmetric\n3 3\n1\n2\n3\n",
+    "array_nonsquare_sym": "%%MatrixMarket matrix array real symmetric\n2 3\n1\n2\n3\n",
+    "complex": "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1 0\n",
+    "hermitian": "%%MatrixMarket matrix coordinate real hermitian\n1 1 1\n1 1 1\n",
+    "bad_banner": "%%MatrixMarkets matrix coordinate real general\n1 1 1\n1 1 1\n",
+    "short_banner": "%%MatrixMarket matrix coordinate real\n1 1 1\n1 1 1\n",
+    "bad_object": "%%MatrixMarket vector coordinate real general\n1 1 1\n1 1 1\n",
+    "bad_format": "%%MatrixMarket matrix sparse real general\n1 1 1\n1 1 1\n",
+    "bad_field": "%%MatrixMarket matrix coordinate double general\n1 1 1\n1 1 1\n",
+    "bad_symmetry": "%%MatrixMarket matrix coordinate real diagonal\n1 1 1\n1 1 1\n",
+    "pattern_array": "%%MatrixMarket matrix array pattern general\n2 2\n",
+    "missing": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1.0\n",
+    "extra": "%%MatrixMarket matrix coordinate real general\n1 1 1\n1 1 1.0\n1 1 2.0\n",
+    "malformed": "%%MatrixMarket matrix coordinate real general\n% filler comment\n3 3 3\n"
+                 "1 1 1.0\n2 oops 2.0\n3 3 3.0\n",
+    "token_count": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n"
+                   "2 2\n",
+    "out_of_range": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n"
+                    "3 1 2.0\n",
+    "zero_index": "%%MatrixMarket matrix coordinate real general\n2 2 1\n0 1 1.0\n",
+    "frac_index": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n"
+                  "1.5 2 2.0\n",
+    "nan_col": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 nan 1.0\n",
+    "bad_size": "%%MatrixMarket matrix coordinate real general\n2 2\n",
+    "size_sign": "%%MatrixMarket matrix coordinate real general\n2 -2 1\n",
+    "no_size": "%%MatrixMarket matrix coordinate real general\n% only comments\n",
+    "empty": "",
+    "underscore": "%%MatrixMarket matrix coordinate real general\n1 1 1\n1 1 1_000\n",
+    "trailing_comment_then_bad": "%%MatrixMarket matrix coordinate real general\n2 2 2\n"
+                                 "1 1 1.0 % note\n2 x 2.0\n",
+    "crlf": "%%MatrixMarket matrix coordinate real general\r\n3 3 3\r\n1 1 1.25\r\n"
+            "2 2 -2\r\n3 3 1e-300\r\n",
+    "tabs_blank_comments": "%%MatrixMarket matrix coordinate real general\n\n%c\n  3\t3  2 \n"
+                           "\n1\t2\t+.5e1 % trailing\n% mid\n\n3 1 -7.\n%end\n",
+    "specials": "%%MatrixMarket matrix coordinate real general\n2 3 5\n1 1 inf\n1 2 -Infinity\n"
+                "2 1 4.9e-324\n2 2 1e400\n2 3 -0.0\n",
+    "lone_cr": "%%MatrixMarket matrix coordinate real general\n2 2 2\r1 1 1.0\r2 2 2.0\n",
+    "unicode_comment": "%%MatrixMarket matrix coordinate real general\n% caf\u00e9\n1 1 1\n"
+                       "1 1 3.5\n",
+    "empty_body": "%%MatrixMarket matrix coordinate real general\n4 5 0\n",
+}
+
+
+def make_mm_fixtures(out_dir):
+    """read_matrix_market on small texts (results or FormatError messages,
+    the path replaced by {path}) and write_matrix_market bytes
+    (io.py:192-259)."""
+    import tempfile
+    from sellkit import FormatError, read_matrix_market, write_matrix_market
+    rng = np.random.default_rng(41)
+    big = []
+    for i in range(4000):
+        big.append(f"{rng.integers(1, 301)} {rng.integers(1, 201)} {rng.standard_normal():.17g}")
+    texts = dict(MM_TEXTS)
+    texts["big"] = "%%MatrixMarket matrix coordinate real general\n300 200 4000\n" + \
+        "\n".join(big) + "\n"
+    tmp = tempfile.mkdtemp()
+    rec = {}
+    for name, text in texts.items():
+        for gz in (False, True):
+            path = os.path.join(tmp, f"{name}.mtx" + (".gz" if gz else ""))
+            if gz:
+                with gzip.open(path, "wb") as fh:
+                    fh.write(text.encode())
+            else:
+                with open(path, "wb") as fh:
+                    fh.write(text.encode())
+            key = name + ("_gz" if gz else "")
+            try:
+                m = read_matrix_market(path)
+                rec[key] = dict(ok=True, n_rows=m.n_rows, n_cols=m.n_cols, rows=m.rows,
+                                cols=m.cols, vals=m.vals)
+            except FormatError as e:
+                rec[key] = dict(ok=False, msg=str(e).replace(path, "{path}"))
+    np.savez_compressed(os.path.join(out_dir, "mm_read.npz"),
+                        names=np.array(sorted(rec)),
+                        **{f"text__{k}": np.frombuffer(v.encode(), np.uint8)
+                           for k, v in texts.items()},
+                        **{f"{k}__{f}": v for k, d in rec.items() for f, v in d.items()})
+    # writer bytes
+    outs = {}
+    cases = {
+        "rand": random_coo(rng, 37, 53, 400),
+        "dups": COOMatrix(3, 3, [2, 0, 2, 1], [1, 0, 1, 2], [0.1, 1e-300, 0.2, -0.0]),
+        "special": COOMatrix(2, 2, [0, 0, 1, 1], [0, 1, 0, 1],
+                             [np.inf, -np.inf, np.nan, 5e-324]),
+        "empty": COOMatrix(3, 2, np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0)),
+    }
+    for name, m in cases.items():
+        path = os.path.join(tmp, f"w_{name}.mtx")
+        write_matrix_market(m, path, comment="written by the reference" if name == "rand"
+                            else None)
+        outs[f"write__{name}"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+        outs[f"coo__{name}__rows"] = m.rows
+        outs[f"coo__{name}__cols"] = m.cols
+        outs[f"coo__{name}__vals"] = m.vals
+        outs[f"coo__{name}__shape"] = np.array(m.shape)
+    np.savez_compressed(os.path.join(out_dir, "mm_write.npz"), **outs)
+
+
 if __name__ == "__main__":
     if "--coo-only" in sys.argv:
         make_coo_fixtures(HERE)
+    elif "--mm-only" in sys.argv:
+        make_mm_fixtures(HERE)
     else:
         main()
         make_coo_fixtures(HERE)
+        make_mm_fixtures(HERE)
