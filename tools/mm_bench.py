@@ -33,9 +33,28 @@ tr = time.perf_counter() - t
 t = time.perf_counter()
 body = mmio._slow_read(p, 3, 3, m.nnz)
 tr_ref = time.perf_counter() - t
+raw = open(p, "rb").read()
+head = mmio._split_header(raw)
+t = time.perf_counter()
+fast = mmio._parse_body(raw, head[3], 3, m.nnz)
+tp = time.perf_counter() - t
+dev = None
+try:
+    import torch
+    if torch.cuda.is_available():
+        sb.read_matrix_market(p, device=0)          # warm-up (CUDA context, pool)
+        t = time.perf_counter()
+        back_d = sb.read_matrix_market(p, device=0)
+        dev = time.perf_counter() - t
+        assert np.array_equal(back_d.vals, m.vals)
+except ImportError:
+    pass
 assert np.array_equal(back.vals, m.vals)
 assert np.array_equal(body[:, 2], m.vals)
 print(f"entries {m.nnz}  file {size / 1e6:.0f} MB  threads {os.cpu_count()}")
 print(f"write: native {tw:.2f} s ({size / tw / 1e6:.0f} MB/s)   np.savetxt {tw_ref:.2f} s")
 print(f"read:  native+canonicalise {tr:.2f} s ({size / tr / 1e6:.0f} MB/s)   "
       f"np.loadtxt body only {tr_ref:.2f} s ({size / tr_ref / 1e6:.0f} MB/s)")
+print(f"       native body parse only {tp:.2f} s ({size / tp / 1e6:.0f} MB/s)"
+      + (f"   read with device canonicalisation {dev:.2f} s ({size / dev / 1e6:.0f} MB/s)"
+         if dev else ""))
