@@ -127,6 +127,56 @@ __device__ __forceinline__ void store_row(T* __restrict__ y, const int32_t* __re
     }
 }
 
+__device__ __forceinline__ double2 ld_x2(const double* p, uint64_t pol) {
+    double2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+        : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+// The U x values of a batch.  When the batch's columns are one consecutive
+// run (stencil rows, windowed rows: c[u] == c[0] + u), U = 8 (the 4-slot
+// instances have no registers to spare for it) and x is 16-byte
+// aligned (vx), they come from U/2 aligned 16-byte loads -- plus one more,
+// predicated, when the run starts at an odd column -- instead of U scalar
+// gathers: the x loads of a warp touch the same lines with fewer
+// instructions, i.e. fewer L1 wavefronts (cfg3 sigma=N is L1-data-pipe bound:
+// 89 % of peak, ~10 lines per scalar gather).  Values are the same doubles,
+// so the sums are unchanged.  Reads stay inside the 16-byte blocks holding
+// x[c[0]] .. x[c[U-1]].
+template <typename T, int U>
+__device__ __forceinline__ void gather_x(T (&xv)[U], const int32_t (&c)[U],
+                                         const T* __restrict__ x, uint64_t pol_x, bool vx) {
+    if constexpr (sizeof(T) == 8 && U == 8) {
+        bool run = vx;
+#pragma unroll
+        for (int u = 1; u < U; ++u) run = run && (c[u] == c[0] + u);
+        if (run) {
+            const bool odd = c[0] & 1;
+            const double* px = x + (c[0] & ~1);
+            double w[U + 2];
+#pragma unroll
+            for (int k = 0; k < U / 2; ++k) {
+                const double2 t = ld_x2(px + 2 * k, pol_x);
+                w[2 * k] = t.x;
+                w[2 * k + 1] = t.y;
+            }
+            w[U] = 0.0;
+            w[U + 1] = 0.0;
+            if (odd) {
+                const double2 t = ld_x2(px + U, pol_x);
+                w[U] = t.x;
+                w[U + 1] = t.y;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = odd ? w[u + 1] : w[u];
+            return;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u], pol_x);
+}
+
 // One row's sum over its first len slots (stride C): U-slot batches -- all
 // val/col loads of the batch, then the U x gathers, then the adds in slot
 // order; a predicated tail batch finishes rows whose length is not a
@@ -134,7 +184,7 @@ __device__ __forceinline__ void store_row(T* __restrict__ y, const int32_t* __re
 template <typename T, int U>
 __device__ __forceinline__ T row_sum(const T* __restrict__ vp, const int32_t* __restrict__ cp,
                                      int64_t C, int len, const T* __restrict__ x,
-                                     uint64_t pol_s, uint64_t pol_x) {
+                                     uint64_t pol_s, uint64_t pol_x, bool vx = false) {
     T sum = T(0);
     int j = 0;
     for (; j + U <= len; j += U) {
@@ -146,8 +196,7 @@ __device__ __forceinline__ T row_sum(const T* __restrict__ vp, const int32_t* __
             c[u] = ld_stream(cp + (int64_t)(j + u) * C, pol_s);
         }
         T xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u], pol_x);
+        gather_x<T, U>(xv, c, x, pol_x, vx);
 #pragma unroll
         for (int u = 0; u < U; ++u) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
     }
@@ -303,7 +352,7 @@ k_spmv_long(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
                                              (size_t)(kThreads / 32) * NS * 2 * kLB) +
                   (size_t)warp * NS * kLB;
     const uint64_t pol_s = make_policy(l2pol & 0xf);
-    const uint64_t pol_x = make_policy(l2pol >> 4);
+    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
     const int64_t chunk = p / C;
     const int64_t base = cs[chunk] + (p - chunk * C);
     const int w = cl[chunk];
@@ -460,7 +509,7 @@ k_spmv_long_grp(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
 
     if (warp > 0) {                                    // ---- producers
         const uint64_t pol_s = make_policy(l2pol & 0xf);
-        const uint64_t pol_x = make_policy(l2pol >> 4);
+        const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
         const int pt = tid - 32;
         const int r = pt & 7;                          // fixed row per producer thread
         const int len = s_len[r];
@@ -575,7 +624,7 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             int long_th, const int32_t* __restrict__ chunk_th, int l2pol) {
     const int64_t C = CC > 0 ? (int64_t)CC : C_rt;
     const uint64_t pol_s = make_policy(l2pol & 0xf);
-    const uint64_t pol_x = make_policy(l2pol >> 4);
+    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
     const int64_t n_long_blocks = LONG ? (n_long + (kThreads / 32) - 1) / (kThreads / 32) : 0;
     if constexpr (LONG) {
         if ((int64_t)blockIdx.x < n_long_blocks) {
@@ -603,7 +652,9 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     }
     const T* vp = val + base;
     const int32_t* cp = col + base;
-    T sum = row_sum<T, U>(vp, cp, C, len, x, pol_s, pol_x);
+    // vector x loads only in the C = 32 instances (the generic-C ones have
+    // no registers to spare for them)
+    T sum = row_sum<T, U>(vp, cp, C, len, x, pol_s, pol_x, CC == 32 && ((l2pol >> 8) & 1));
     if (skip_pad && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
     store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
 }
@@ -621,7 +672,7 @@ k_spmv_sell_sweep(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl
                   const int32_t* __restrict__ order, int64_t c0, int64_t c1, int64_t n_rows,
                   int l2pol) {
     const uint64_t pol_s = make_policy(l2pol & 0xf);
-    const uint64_t pol_x = make_policy(l2pol >> 4);
+    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
     const int lane = threadIdx.x & 31;
     const int64_t n_warps = (int64_t)gridDim.x * (kThreads / 32);
     int64_t c = c0 + (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
@@ -762,8 +813,16 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         const char* e = getenv("SELLB_L2POL");
         return e ? (int)strtol(e, nullptr, 0) : -1;
     }();
-    const int l2pol = l2pol_env >= 0 ? l2pol_env
-                      : ((int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20);
+    // bit 8: vector x loads for consecutive-column batches (gather_x);
+    // needs a 16-byte aligned x.  SELLB_VX=0 disables.
+    static const int vx_env = [] {
+        const char* e = getenv("SELLB_VX");
+        return e ? atoi(e) : 1;
+    }();
+    const int vx = (vx_env && ((uintptr_t)x & 15) == 0) ? 0x100 : 0;
+    const int l2pol = (l2pol_env >= 0 ? l2pol_env
+                       : ((int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20))
+                      | vx;
     // slots batched per load round: 8 for fp32 (half the bytes per slot),
     // long rows (N_nzr >= 24) and skewed matrices (some chunk wider than 64),
     // else 4 (measured, tools/ab_env.sh: cfg2 f32 1230 -> 1377 GF/s, cfg3
