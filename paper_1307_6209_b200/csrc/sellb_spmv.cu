@@ -950,7 +950,18 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         const char* e = getenv("SELLB_LONG_REST");
         return e ? atoi(e) : 0;
     }();
-    if (n_long && long_mode != 0 && (m->n_groups || rest_sep)) {
+    // isolated long rows (not in a row group) by the TMA kernel
+    // (sellb_tma_long.cu): opt-in, SELLB_LONG_TMA=1.  Measured slower than
+    // the fused role (cfg4 sigma=1 304 -> 280 GF/s): each 16-byte box row of
+    // a row 256 bytes from the next pulls a whole 128-byte line from DRAM
+    // (554 MB read for 25 MB of long-row data, ncu), so the kernel is
+    // DRAM-transaction bound at 89 us vs 42 us for the rest of the matrix.
+    static const int rest_tma_env = [] {
+        const char* e = getenv("SELLB_LONG_TMA");
+        return e ? atoi(e) : 0;
+    }();
+    const bool rest_tma = rest_tma_env && !rest_sep && m->n_rest && long_tma_possible(m);
+    if (n_long && long_mode != 0 && (m->n_groups || rest_sep || rest_tma)) {
         sellb_mat* mm = const_cast<sellb_mat*>(m);
         std::unique_lock<std::mutex> lk(mm->long_mu, std::defer_lock);
         cudaStream_t ls = st;
@@ -1023,6 +1034,11 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         // fused warp-per-row role (below); SELLB_LONG_REST=1 sends them to
         // the pipelined warp-per-row kernel instead (measured slower: cfg4
         // sigma=1 117 vs 165 us)
+        bool rest_fused = !rest_sep;
+        if (rest_tma) {
+            if (launch_long_tma(m, x, y, p0, p1, ACC, ORD, m->long_rest, m->n_rest, l2pol, ls))
+                rest_fused = false;
+        }
         if (m->n_rest && rest_sep) {
             if (long_d == 3) SELLB_LONG_LAUNCH(3, 1, m->long_rest, m->n_rest);
             else if (long_d == 6) SELLB_LONG_LAUNCH(6, 3, m->long_rest, m->n_rest);
@@ -1036,8 +1052,8 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         // template), no long-role blocks
         grid = (unsigned)grid_for(rows, kThreads);
         if (long_mode == 2) SELLB_CU(cudaEventRecord(mm->ev_join, ls));
-        const int32_t* rest = rest_sep ? nullptr : m->long_rest;
-        const int64_t n_rest = rest_sep ? 0 : m->n_rest;
+        const int32_t* rest = rest_fused ? m->long_rest : nullptr;
+        const int64_t n_rest = rest_fused ? m->n_rest : 0;
         grid += (unsigned)((n_rest + kThreads / 32 - 1) / (kThreads / 32));
         if (u8) SELLB_LAUNCH(8, true, rest, n_rest, m->long_th);
         else SELLB_LAUNCH(4, true, rest, n_rest, m->long_th);

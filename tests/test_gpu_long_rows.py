@@ -1,7 +1,9 @@
-"""GPU parity of the long-row paths (sellb_spmv.cu): the row-group kernel
-(k_spmv_long_grp, 8-row groups of sorted chunks, producer/chain warps), the
-fused warp-per-row role and the pipelined warp-per-row kernel, under every
-launch mode (SELLB_LONG_MODE 0/1/2), batch size and wave cap.
+"""GPU parity of the long-row paths (sellb_spmv.cu, sellb_tma_long.cu): the
+row-group kernel (k_spmv_long_grp, 8-row groups of sorted chunks,
+producer/chain warps), the TMA kernel for isolated long rows
+(k_spmv_long_tma), the fused warp-per-row role and the pipelined warp-per-row
+kernel, under every launch mode (SELLB_LONG_MODE 0/1/2), batch size and wave
+cap.
 
 Matrices are built so the groups are full, partial (4..7 long rows next to
 shorter ones), or sparse (< 4 long rows: warp-per-row), chunks are
@@ -106,6 +108,8 @@ MODES = [
     {"SELLB_LONG_MODE": "2", "SELLB_GRP_CTAS": "3", "SELLB_LONG_REST": "1"},
     {"SELLB_LONG_MODE": "1", "SELLB_LONG_GRP": "0", "SELLB_LONG_REST": "1",
      "SELLB_LONG_D": "3"},
+    {"SELLB_LONG_MODE": "2", "SELLB_LONG_TMA": "0"},            # isolated rows fused
+    {"SELLB_LONG_MODE": "1", "SELLB_LONG_GRP": "0"},            # every long row by TMA
 ]
 
 
