@@ -877,6 +877,15 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
                 m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol);                       \
         }                                                                                       \
     } while (0)
+    // L2 fetch granularity hint (SELLB_L2FETCH=<bytes>, A/B knob; device-wide,
+    // so only on request): smaller fetches for scattered sectors
+    static const int l2fetch = [] {
+        const char* e = getenv("SELLB_L2FETCH");
+        const int v = e ? atoi(e) : -1;
+        if (v >= 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)v);
+        return v;
+    }();
+    (void)l2fetch;
     // x as a persisting L2 window (SELLB_L2PERSIST=1, A/B knob): the driver
     // sets aside up to the device's persisting-L2 maximum for it
     static const int persist_env = [] {
