@@ -540,7 +540,8 @@ def run_ours(args):
     if not args.skip_cpu:
         cpu = wl["cpu"](args.cpu_budget)
 
-    traffic = load_profile_traffic(f"{args.config}_s{sigma}_{args.dtype}")
+    traffic = load_profile_traffic(f"{args.config}_s{sigma}_{args.dtype}") if args.C == 32 \
+        else None
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup,
