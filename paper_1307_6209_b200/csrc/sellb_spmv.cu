@@ -700,6 +700,69 @@ k_spmv_sell_sweep(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl
     }
 }
 
+// Warp-level variant for very short chunks (C = 32, every chunk at most W
+// slots wide: diagonal / tridiagonal-like rows): one warp owns K consecutive
+// chunks, lane = row in each, and issues all K chunks' metadata loads, then
+// all K*W val/col loads, then all x gathers before the first add -- K times
+// the bytes in flight of the one-chunk-per-warp grid, whose rows carry too
+// little data to cover three dependent DRAM round trips (16 M rows of width
+// 1: 3.7 TB/s).  Each row is still summed in slot order from +0.0.
+template <typename T, bool SKIP, bool ACC, int ORD, int K, int W>
+__global__ void __launch_bounds__(kThreads)
+k_spmv_sell_short(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+                  const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+                  const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+                  const int32_t* __restrict__ order, int64_t c0, int64_t c1, int64_t n_rows,
+                  int l2pol) {
+    const uint64_t pol_s = make_policy(l2pol & 0xf);
+    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
+    const int lane = threadIdx.x & 31;
+    const int64_t cb = c0 + ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * K;
+    if (cb >= c1) return;
+    int64_t base[K];
+    int w[K], len[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int64_t c = cb + k;
+        base[k] = 0;
+        w[k] = 0;
+        len[k] = 0;
+        if (c < c1) {
+            base[k] = cs[c];
+            w[k] = cl[c];
+            len[k] = SKIP ? rl[c * 32 + lane] : w[k];
+        }
+    }
+    T v[K][W];
+    int32_t ci[K][W];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            v[k][j] = T(0);
+            ci[k][j] = 0;
+            if (j < len[k]) {
+                v[k][j] = ld_stream(val + base[k] + j * 32 + lane, pol_s);
+                ci[k][j] = ld_stream(col + base[k] + j * 32 + lane, pol_s);
+            }
+        }
+    T xv[K][W];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int j = 0; j < W; ++j) xv[k][j] = j < len[k] ? ld_x(x + ci[k][j], pol_x) : T(0);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (cb + k >= c1) break;
+        T sum = T(0);
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (j < len[k]) sum = Arith<T>::add(sum, Arith<T>::mul(v[k][j], xv[k][j]));
+        if (SKIP && len[k] < w[k]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+        store_row<T, ACC, ORD>(y, order, (cb + k) * 32 + lane, n_rows, sum);
+    }
+}
+
 // Chunk-list variant (multi-GPU interior / boundary passes): block b handles
 // kThreads consecutive stored rows of chunk ids[...]; generic C.
 template <typename T, bool SKIP, bool ACC>
@@ -921,6 +984,41 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         const char* e = getenv("SELLB_SWEEP");
         return e ? atoi(e) : 0;
     }();
+    // very short chunks (every chunk <= 2 slots): K chunks per warp
+    // (k_spmv_sell_short).  Measured on 16 M rows (tools/short_ab.sh): width 1
+    // 126 -> 74 us (K = 4, 6.3 TB/s), width 2 138 -> 111 us (K = 2); width 3
+    // gains nothing (152 vs 156 us) and stays on the default grid.
+    // SELLB_SHORT=0 disables, SELLB_SHORT_K=2|4|8 forces K.
+    static const int short_env = [] {
+        const char* e = getenv("SELLB_SHORT");
+        return e ? atoi(e) : 1;
+    }();
+    static const int short_k_env = [] {
+        const char* e = getenv("SELLB_SHORT_K");
+        return e ? atoi(e) : 0;
+    }();
+    const int short_k = short_k_env ? short_k_env : (m->max_cl <= 1 ? 4 : 2);
+    if (CC == 32 && !n_long && short_env && m->max_cl <= (short_k_env ? 3 : 2) &&
+        sweep_env != 1) {
+        const int64_t chunks = (p1 - p0) / 32;
+#define SELLB_SHORT_LAUNCH(KK, WW)                                                              \
+    k_spmv_sell_short<T, SKIP, ACC, ORD, KK, WW>                                                \
+        <<<(unsigned)((chunks + (kThreads / 32) * KK - 1) / ((kThreads / 32) * KK)), kThreads, 0, \
+           st>>>(m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,   \
+                 p0 / 32, p1 / 32, m->n_rows, l2pol)
+#define SELLB_SHORT_W(KK)                                                                       \
+    do {                                                                                        \
+        if (m->max_cl <= 1) SELLB_SHORT_LAUNCH(KK, 1);                                          \
+        else if (m->max_cl == 2) SELLB_SHORT_LAUNCH(KK, 2);                                     \
+        else SELLB_SHORT_LAUNCH(KK, 3);                                                         \
+    } while (0)
+        if (short_k == 2) SELLB_SHORT_W(2);
+        else if (short_k == 8) SELLB_SHORT_W(8);
+        else SELLB_SHORT_W(4);
+#undef SELLB_SHORT_W
+#undef SELLB_SHORT_LAUNCH
+        return 0;
+    }
     const bool sweep = CC == 32 && !n_long && sweep_env == 1;
     if (sweep) {
         static const int sms = [] {
