@@ -127,6 +127,13 @@ __device__ __forceinline__ void store_row(T* __restrict__ y, const int32_t* __re
     }
 }
 
+#ifndef SELLB_VX256
+#define SELLB_VX256 0
+#endif
+__device__ __forceinline__ void ld_x4(const double* p, uint64_t pol, double* w) {
+    asm("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+        : "=d"(w[0]), "=d"(w[1]), "=d"(w[2]), "=d"(w[3]) : "l"(p), "l"(pol));
+}
 __device__ __forceinline__ double2 ld_x2(const double* p, uint64_t pol) {
     double2 v;
     asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
@@ -152,6 +159,20 @@ __device__ __forceinline__ void gather_x(T (&xv)[U], const int32_t (&c)[U],
 #pragma unroll
         for (int u = 1; u < U; ++u) run = run && (c[u] == c[0] + u);
         if (run) {
+#if SELLB_VX256
+            // 32-byte loads: 2 (aligned run) or 3 per 8 slots
+            const int off = c[0] & 3;
+            const double* px = x + (c[0] & ~3);
+            double w[U + 4];
+#pragma unroll
+            for (int k = 0; k < U / 4; ++k) ld_x4(px + 4 * k, pol_x, w + 4 * k);
+#pragma unroll
+            for (int k = U; k < U + 4; ++k) w[k] = 0.0;
+            if (off) ld_x4(px + U, pol_x, w + U);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                xv[u] = off == 0 ? w[u] : off == 1 ? w[u + 1] : off == 2 ? w[u + 2] : w[u + 3];
+#else
             const bool odd = c[0] & 1;
             const double* px = x + (c[0] & ~1);
             double w[U + 2];
@@ -170,6 +191,7 @@ __device__ __forceinline__ void gather_x(T (&xv)[U], const int32_t (&c)[U],
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) xv[u] = odd ? w[u + 1] : w[u];
+#endif
             return;
         }
     }

@@ -7,9 +7,9 @@ NAME=$1; DEFS=$2
 D=paper_1307_6209_b200/csrc
 B=$D/build_$NAME
 mkdir -p $B
-for f in sellb_util sellb_build sellb_spmv sellb_gen sellb_tma; do
+for f in $(cd $D && ls *.cu | sed 's/\.cu$//'); do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false \
-       -Xcompiler -fPIC,-O2 $DEFS -c $D/$f.cu -o $B/$f.o &
+       -Xcompiler -fPIC,-O2 -Xptxas -v $DEFS -c $D/$f.cu -o $B/$f.o 2> $B/$f.ptxas.log &
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_1307_6209_b200/libsellb200_$NAME.so \
