@@ -179,12 +179,22 @@ def cpu_reference_run(o, x, budget_s=10.0, threads=None, n_chunks=None):
 
 
 def host_cpu_desc():
+    """CPU model, logical CPUs and last-level cache from lscpu."""
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
-        model = [l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")]
-        return model[0] if model else "unknown"
     except OSError:
         return "unknown"
+    kv = {}
+    for line in out.splitlines():
+        if ":" in line:
+            k, v = line.split(":", 1)
+            kv[k.strip()] = v.strip()
+    desc = kv.get("Model name", "unknown")
+    if kv.get("CPU(s)"):
+        desc += f", {kv['CPU(s)']} logical CPUs"
+    if kv.get("L3 cache"):
+        desc += f", L3 {kv['L3 cache']}"
+    return desc
 
 
 # ---------------------------------------------------------------------------
@@ -356,7 +366,11 @@ def host_workload(args, dt_np):
                                args.sigma)
         gf, kind, cores, sample, _ = cpu_reference_run(o, x.astype(np.float64),
                                                        budget_s=budget)
+        # the same kernel on one thread (T = 1 and T = all)
+        gf1, _, _, _, _ = cpu_reference_run(o, x.astype(np.float64),
+                                            budget_s=min(4.0, budget / 3), threads=1)
         return {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": kind,
+                "value_1thread": round(gf1, 4),
                 "sample": sample + f"; host {host_cpu_desc()}"}
 
     return {"sell": s, "desc": desc, "x": x, "build_s": build_s, "parity": parity, "cpu": cpu,
