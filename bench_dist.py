@@ -93,7 +93,7 @@ def bench_main(args):
     st = torch.cuda.current_stream(device)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    launches0 = ds.engine.launches
+    launches0 = ds.engine.lib.sellb_launch_count()
     sampler = args.clock_sampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -114,7 +114,7 @@ def bench_main(args):
     tdist.all_reduce(nz_t)
     par_t = torch.tensor([1.0 if parity in (True, None) else 0.0], device=device)
     tdist.all_reduce(par_t, op=tdist.ReduceOp.MIN)
-    launches = ds.engine.launches - launches0
+    launches = ds.engine.lib.sellb_launch_count() - launches0
 
     # e2e through host buffers: each rank's x slice H2D from pinned memory,
     # the distributed product, y slice D2H into pinned memory, every step

@@ -245,6 +245,11 @@ int sellb_mm_parse_body(const char* text, int64_t len, int32_t width, int64_t ma
 int sellb_mm_format_body(const int64_t* rows, const int64_t* cols, const double* vals,
                          int64_t n, char* out, int64_t cap, int64_t* used, int32_t n_threads);
 
+/* Process-wide number of compute-path kernel launches so far (SpMV roles,
+ * long-row kernels, halo gather/scatter, pad fix-up, CRS kernels, L2 flush,
+ * membench kernels): the bench's gpu_launches is a difference of two reads. */
+int64_t sellb_launch_count(void);
+
 /* Pinned host buffers for the end-to-end path. */
 int sellb_host_alloc(size_t bytes, void** out);
 int sellb_host_free(void* p);

@@ -145,6 +145,10 @@ bool long_tma_possible(const sellb_mat* m);
 
 inline int64_t grid_for(int64_t n, int threads) { return (n + threads - 1) / threads; }
 
+// process-wide count of compute-path kernel launches (sellb_launch_count)
+void count_launches(int n = 1);
+long long launch_counter();
+
 }  // namespace sellb
 
 #define SELLB_CU(call)                                                                  \

@@ -961,6 +961,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
                 m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
                 m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol);                       \
         }                                                                                       \
+        count_launches();                                                                       \
     } while (0)
     // L2 fetch granularity hint (SELLB_L2FETCH=<bytes>, A/B knob; device-wide,
     // so only on request): smaller fetches for scattered sectors
@@ -1037,6 +1038,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         if (short_k == 2) SELLB_SHORT_W(2);
         else if (short_k == 8) SELLB_SHORT_W(8);
         else SELLB_SHORT_W(4);
+        count_launches();
 #undef SELLB_SHORT_W
 #undef SELLB_SHORT_LAUNCH
         return 0;
@@ -1057,6 +1059,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         p1 / 32, m->n_rows, l2pol)
         if (m->max_cl <= 6) SELLB_SWEEP_LAUNCH(6);
         else SELLB_SWEEP_LAUNCH(8);
+        count_launches();
 #undef SELLB_SWEEP_LAUNCH
         return 0;
     }
@@ -1128,6 +1131,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
             <<<(unsigned)(((NL) + kThreads / 32 - 1) / (kThreads / 32)), kThreads, smem_, ls>>>( \
                 m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
                 m->C, p0, p1, m->n_rows, LIST, NL, l2pol);                                      \
+        count_launches();                                                                       \
     } while (0)
 #define SELLB_GRP_LAUNCH(DD, EE, TT)                                                            \
     do {                                                                                        \
@@ -1142,6 +1146,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
             k_spmv_long_grp<T, ACC, ORD, DD, EE, TT><<<(unsigned)ng_, kGT, smem_, ls>>>(        \
                 m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
                 m->C, p0, p1, m->n_rows, m->long_groups + g_, ng_, m->chunk_th, l2pol);         \
+            count_launches();                                                                   \
         }                                                                                       \
     } while (0)
         static const int grp_ctas = [] {
@@ -1290,6 +1295,7 @@ int launch_spmv_list(const sellb_mat* m, const int32_t* ids, int64_t n_ids, cons
         if (skip) { if (accumulate) SELLB_LIST(double, true, true); else SELLB_LIST(double, true, false); }
         else { if (accumulate) SELLB_LIST(double, false, true); else SELLB_LIST(double, false, false); }
     }
+    count_launches();
 #undef SELLB_LIST
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
@@ -1311,6 +1317,7 @@ int launch_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val, int
         else { if (accumulate) SELLB_CRS(k_spmv_crs, double, true); else SELLB_CRS(k_spmv_crs, double, false); }
     }
 #undef SELLB_CRS
+    count_launches();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return set_error(SELLB_ERESOURCE, "crs launch failed: %s", cudaGetErrorString(e));
@@ -1370,6 +1377,7 @@ int sellb_pad_fixup(const sellb_mat* m, const void* x0, void* y, void* stream) {
     else
         k_pad_fixup<double><<<grid, kThreads, 0, st>>>(m->cl, m->rl, m->C, m->n_pad,
                                                       (const double*)x0, (double*)y);
+    count_launches();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return set_error(SELLB_ERESOURCE, "fix-up launch failed: %s", cudaGetErrorString(e));

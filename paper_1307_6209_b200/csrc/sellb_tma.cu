@@ -204,6 +204,7 @@ int launch_spmv_tma(const sellb_mat* m, const void* x, void* y, int64_t c0, int6
     }
 #undef SELLB_TMA
 #undef SELLB_TMA_U
+    count_launches();
     return 1;
 }
 

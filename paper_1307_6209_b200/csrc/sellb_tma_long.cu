@@ -4,9 +4,12 @@
 //
 // Such a row's slot j lives at cs + j*C + r: 256 bytes (fp64, C = 32) apart,
 // so every warp-wide load of the warp-per-row role touches 32 different lines
-// and the L1 data pipe, not DRAM, sets the pace (cfg4 sigma=1: 1024 rows of
-// 2048 slots took ~120 us of a 120 us SpMV while the rest of the matrix needs
-// 40 us).  Here val and col are 2-D tensors [slots / C][C]; one TMA box of
+// (cfg4 sigma=1: 1024 rows of 2048 slots took ~120 us of a 120 us SpMV while
+// the rest of the matrix needs 40 us).  Opt-in (SELLB_LONG_TMA=1): measured
+// slower than the fused role -- every 16-byte box row still costs a 128-byte
+// DRAM line (554 MB read for 25 MB of data, ncu), so these rows are bound by
+// DRAM transactions however they are fetched.  Here val and col are 2-D
+// tensors [slots / C][C]; one TMA box of
 // {16 bytes of rows} x {SB slots} per array and batch lands the row (and its
 // neighbours in the same 16 bytes) in shared memory, completing on an
 // mbarrier -- no LSU wavefronts, D batches in flight per warp.  The x values
@@ -269,6 +272,7 @@ int launch_long_tma(const sellb_mat* m, const void* x, void* y, int64_t p0, int6
     }
 #undef SELLB_LT_O
 #undef SELLB_LT
+    count_launches();
     return 1;
 }
 

@@ -4,6 +4,8 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <atomic>
+
 #include "sellb_internal.cuh"
 
 namespace sellb {
@@ -35,6 +37,10 @@ void retain_pool_memory() {
     cudaGetLastError();
     done[dev] = true;
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_counter() { return g_launches.load(std::memory_order_relaxed); }
 
 }  // namespace sellb
 
@@ -163,6 +169,7 @@ int sellb_read_sum(const double* a, int64_t n, double* out_host, void* stream) {
     SELLB_CU(res.alloc(sizeof(double), st));
     k_read_sum<<<blocks, 256, 0, st>>>(a, n, part.as<double>());
     k_sum_partials<<<1, 1024, 0, st>>>(part.as<double>(), blocks, res.as<double>());
+    count_launches(2);
     SELLB_CU(cudaGetLastError());
     if (out_host) {
         SELLB_CU(cudaMemcpyAsync(out_host, res.p, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -175,9 +182,12 @@ int sellb_copy(const double* src, double* dst, int64_t n, void* stream) {
     clear_error();
     cudaStream_t st = (cudaStream_t)stream;
     k_copy<<<grid_fill(), 256, 0, st>>>(src, dst, n);
+    count_launches();
     SELLB_CU(cudaGetLastError());
     return 0;
 }
+
+int64_t sellb_launch_count(void) { return sellb::launch_counter(); }
 
 int sellb_l2_flush(void* scratch, int64_t bytes, void* stream) {
     clear_error();
@@ -190,6 +200,7 @@ int sellb_l2_flush(void* scratch, int64_t bytes, void* stream) {
     //    clean lines, so the next kernel does not pay for writing back the
     //    flush's dirty lines inside its own timed region
     k_touch<<<grid_fill(), 256, 0, st>>>((uint4*)scratch, bytes / 16, v);
+    count_launches(2);
     k_sweep<<<grid_fill(), 256, 0, st>>>((const uint4*)scratch, bytes / 32, v - 1,
                                          (unsigned*)scratch);
     SELLB_CU(cudaGetLastError());
@@ -206,6 +217,7 @@ int sellb_gather(const void* x, const int32_t* idx, void* out, int64_t n, int32_
         k_gather<float><<<g, 256, 0, st>>>((const float*)x, idx, (float*)out, n);
     else
         k_gather<double><<<g, 256, 0, st>>>((const double*)x, idx, (double*)out, n);
+    count_launches();
     SELLB_CU(cudaGetLastError());
     return 0;
 }
@@ -220,6 +232,7 @@ int sellb_scatter(const void* in, const int32_t* idx, void* x, int64_t n, int32_
         k_scatter<float><<<g, 256, 0, st>>>((const float*)in, idx, (float*)x, n);
     else
         k_scatter<double><<<g, 256, 0, st>>>((const double*)in, idx, (double*)x, n);
+    count_launches();
     SELLB_CU(cudaGetLastError());
     return 0;
 }
