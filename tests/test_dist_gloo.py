@@ -7,7 +7,6 @@ GPU.  The concatenated y must equal the single-process oracle product
 bit for bit, including the NaN rows a non-finite x[0] produces.
 """
 
-import os
 import socket
 
 import numpy as np

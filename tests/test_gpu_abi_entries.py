@@ -2,8 +2,6 @@
 the stateless reference-signature range kernel, device CRS kernels, the
 membench kernels, and int64 slot offsets beyond 2^31."""
 
-import ctypes
-
 import numpy as np
 import pytest
 

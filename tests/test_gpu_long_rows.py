@@ -22,9 +22,8 @@ import sys
 import numpy as np
 import pytest
 
-import oracle
 import paper_1307_6209_b200 as sb
-from paper_1307_6209_b200 import CRSMatrix, kernels_cuda
+from paper_1307_6209_b200 import CRSMatrix
 
 pytestmark = pytest.mark.gpu
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
