@@ -156,7 +156,7 @@ unsigned grid_of(int64_t n) {
 }
 
 template <typename IdxT>
-int canonicalize(const int64_t* rows, const int64_t* cols, const double* vals, int64_t nnz,
+int canonicalize(const double* vals, int64_t nnz,
                  int64_t n_rows, int cbits, int rbits, bool sorted, int64_t* rpt_d,
                  int32_t* col_d, double* val_d, int64_t* nnz_out, DBuf& d_keys,
                  cudaStream_t st) {
@@ -296,9 +296,9 @@ int sellb_coo_to_crs(const int64_t* rows, const int64_t* cols, const double* val
         }
         const bool sorted = (uint32_t)hf[2] == 0u;
         const int rc = nnz < (1ll << 32)
-            ? canonicalize<uint32_t>(rows_d, cols_d, vals_d, nnz, n_rows, cbits, rbits, sorted,
+            ? canonicalize<uint32_t>(vals_d, nnz, n_rows, cbits, rbits, sorted,
                                      rpt_d, col_d, val_d, nnz_out, d_keys, st)
-            : canonicalize<uint64_t>(rows_d, cols_d, vals_d, nnz, n_rows, cbits, rbits, sorted,
+            : canonicalize<uint64_t>(vals_d, nnz, n_rows, cbits, rbits, sorted,
                                      rpt_d, col_d, val_d, nnz_out, d_keys, st);
         if (rc) return rc;
     }

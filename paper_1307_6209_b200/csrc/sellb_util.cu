@@ -202,7 +202,7 @@ int sellb_l2_flush(void* scratch, int64_t bytes, void* stream) {
     k_touch<<<grid_fill(), 256, 0, st>>>((uint4*)scratch, bytes / 16, v);
     count_launches(2);
     k_sweep<<<grid_fill(), 256, 0, st>>>((const uint4*)scratch, bytes / 32, v - 1,
-                                         (unsigned*)scratch);
+                                         (unsigned*)((char*)scratch + bytes - 16));
     SELLB_CU(cudaGetLastError());
     return 0;
 }
