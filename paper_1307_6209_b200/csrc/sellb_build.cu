@@ -207,6 +207,9 @@ void free_mat_arrays(sellb_mat* m) {
     cudaFree(m->chunk_th);
     cudaFree(m->long_groups);
     cudaFree(m->long_rest);
+    cudaFree(m->side_off);
+    cudaFree(m->side_col);
+    cudaFree(m->side_val);
     if (m->pipe_ready) {
         cudaStreamDestroy(m->s_h2d);
         cudaStreamDestroy(m->s_comp);
@@ -274,6 +277,27 @@ int choose_variant(sellb_mat* m, cudaStream_t st, double* beta_eff_out, int64_t*
     return 0;
 }
 
+// long-row side table: warp k copies stored row rows[k] (slots j < rl, C
+// apart in the SELL arrays) to side_*[off[k] + j]
+template <typename T>
+__global__ void k_side_fill(const int64_t* __restrict__ cs, const int32_t* __restrict__ col,
+                            const T* __restrict__ val, const int32_t* __restrict__ rows,
+                            int64_t n, int64_t C, const int32_t* __restrict__ rl,
+                            const int64_t* __restrict__ off, int32_t* __restrict__ side_col,
+                            T* __restrict__ side_val) {
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (k >= n) return;
+    const int64_t p = rows[k];
+    const int64_t chunk = p / C;
+    const int64_t base = cs[chunk] + (p - chunk * C);
+    const int len = rl[p];
+    for (int j = lane; j < len; j += 32) {
+        side_col[off[k] + j] = col[base + (int64_t)j * C];
+        side_val[off[k] + j] = val[base + (int64_t)j * C];
+    }
+}
+
 // Rows longer than the threshold go to the kernel's warp-per-row role.
 // Default threshold 256 slots (SELLB_LONG_TH overrides; <= 0 disables).
 int build_long_rows(sellb_mat* m, cudaStream_t st) {
@@ -281,6 +305,12 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     cudaFree(m->chunk_th);
     cudaFree(m->long_groups);
     cudaFree(m->long_rest);
+    cudaFree(m->side_off);
+    cudaFree(m->side_col);
+    cudaFree(m->side_val);
+    m->side_off = nullptr;
+    m->side_col = nullptr;
+    m->side_val = nullptr;
     m->long_rows = nullptr;
     m->chunk_th = nullptr;
     m->long_groups = nullptr;
@@ -371,6 +401,32 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
         if (int rc = alloc_dev((void**)&m->long_rest, rest.size() * 4)) return rc;
         SELLB_CU(cudaMemcpyAsync(m->long_rest, rest.data(), rest.size() * 4,
                                  cudaMemcpyHostToDevice, st));
+    }
+    // side table for the rest rows (bounded: at most a quarter of the
+    // matrix's entries)
+    const bool want_side = !(getenv("SELLB_LONG_SIDE") && atoi(getenv("SELLB_LONG_SIDE")) == 0);
+    if (want_side && !rest.empty()) {
+        std::vector<int64_t> off(rest.size() + 1, 0);
+        for (size_t k = 0; k < rest.size(); ++k) off[k + 1] = off[k] + h_rl[rest[k]];
+        const int64_t total = off.back();
+        if (total > 0 && total * 4 <= std::max<int64_t>(m->nnz, 1)) {
+            const size_t vs = vsize(m->dtype);
+            if (int rc = alloc_dev((void**)&m->side_off, off.size() * 8)) return rc;
+            if (int rc = alloc_dev((void**)&m->side_col, total * 4)) return rc;
+            if (int rc = alloc_dev(&m->side_val, total * vs)) return rc;
+            SELLB_CU(cudaMemcpyAsync(m->side_off, off.data(), off.size() * 8,
+                                     cudaMemcpyHostToDevice, st));
+            const unsigned grid = (unsigned)grid_for((int64_t)rest.size() * 32, 256);
+            if (m->dtype == SELLB_F32)
+                k_side_fill<float><<<grid, 256, 0, st>>>(
+                    m->cs, m->col, (const float*)m->val, m->long_rest, (int64_t)rest.size(),
+                    m->C, m->rl, m->side_off, m->side_col, (float*)m->side_val);
+            else
+                k_side_fill<double><<<grid, 256, 0, st>>>(
+                    m->cs, m->col, (const double*)m->val, m->long_rest, (int64_t)rest.size(),
+                    m->C, m->rl, m->side_off, m->side_col, (double*)m->side_val);
+            SELLB_CU(cudaGetLastError());
+        }
     }
     SELLB_CU(cudaStreamSynchronize(st));
     m->n_long = (int64_t)rows.size();

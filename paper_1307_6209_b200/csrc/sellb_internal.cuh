@@ -51,6 +51,13 @@ struct sellb_mat {
     int64_t n_groups = 0;
     int32_t* long_rest = nullptr;
     int64_t n_rest = 0;
+    // long-row side table: the long_rest rows' values / indices stored
+    // contiguously row after row (side_off[k] = start of long_rest[k]), so the
+    // warp-per-row role reads them coalesced instead of one 8-byte element per
+    // 128-byte DRAM line in the padded SELL layout (SELLB_LONG_SIDE=0: off)
+    int64_t* side_off = nullptr;
+    int32_t* side_col = nullptr;
+    void* side_val = nullptr;
     int32_t long_th = 0x7fffffff;     // chunks wider than this may hold long rows
     int32_t* chunk_th = nullptr;      // per chunk: rows longer than this are long
     // long-row kernel on a side stream, forked from / joined into the

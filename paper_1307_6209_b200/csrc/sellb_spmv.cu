@@ -255,21 +255,17 @@ __device__ __forceinline__ T row_sum(const T* __restrict__ vp, const int32_t* __
 // never be -0.0), so the chain needs no predicate.  kSeg*32 slots per batch.
 constexpr int kSeg = 4;
 
+// vp / cp: the row's first value / index, `stride` elements apart (C in the
+// SELL arrays, 1 in the long-row side table); w: the chunk width (padding
+// fix-up)
 template <typename T, bool ACC, int ORD>
-__device__ __forceinline__ void long_row(const int64_t* __restrict__ cs,
-                                         const int32_t* __restrict__ cl,
-                                         const int32_t* __restrict__ rl,
-                                         const int32_t* __restrict__ col,
-                                         const T* __restrict__ val, const T* __restrict__ x,
-                                         T* __restrict__ y, const int32_t* __restrict__ order,
-                                         int64_t C, int64_t p, int64_t n_rows, int lane,
-                                         uint64_t pol_s, uint64_t pol_x, T* __restrict__ stage) {
-    const int64_t chunk = p / C;
-    const int64_t base = cs[chunk] + (p - chunk * C);
-    const int w = cl[chunk];
-    const int len = rl[p];
-    const T* vp = val + base;
-    const int32_t* cp = col + base;
+__device__ __forceinline__ void long_row_at(const T* __restrict__ vp,
+                                            const int32_t* __restrict__ cp, int64_t stride,
+                                            int len, int w, const T* __restrict__ x,
+                                            T* __restrict__ y, const int32_t* __restrict__ order,
+                                            int64_t p, int64_t n_rows, int lane, uint64_t pol_s,
+                                            uint64_t pol_x, T* __restrict__ stage) {
+    const int64_t C = stride;
     T sum = T(0);
     for (int j0 = 0; j0 < len; j0 += 32 * kSeg) {
         T prod[kSeg];
@@ -643,7 +639,9 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
             const int32_t* __restrict__ order, int64_t C_rt, int64_t p0, int64_t p1,
             int64_t n_rows, const int32_t* __restrict__ long_rows, int64_t n_long,
-            int long_th, const int32_t* __restrict__ chunk_th, int l2pol) {
+            int long_th, const int32_t* __restrict__ chunk_th, int l2pol,
+            const int64_t* __restrict__ side_off, const int32_t* __restrict__ side_col,
+            const T* __restrict__ side_val) {
     const int64_t C = CC > 0 ? (int64_t)CC : C_rt;
     const uint64_t pol_s = make_policy(l2pol & 0xf);
     const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
@@ -655,8 +653,18 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             if (k >= n_long) return;
             const int64_t p = long_rows[k];
             if (p < p0 || p >= p1) return;
-            long_row<T, ACC, ORD>(cs, cl, rl, col, val, x, y, order, C, p, n_rows,
-                                  threadIdx.x & 31, pol_s, pol_x, stage[threadIdx.x >> 5]);
+            const int64_t chunk = p / C;
+            if (side_off) {             // the row, contiguous (long-row side table)
+                const int64_t o = side_off[k];
+                long_row_at<T, ACC, ORD>(side_val + o, side_col + o, 1, rl[p], cl[chunk], x, y,
+                                         order, p, n_rows, threadIdx.x & 31, pol_s, pol_x,
+                                         stage[threadIdx.x >> 5]);
+            } else {
+                const int64_t base = cs[chunk] + (p - chunk * C);
+                long_row_at<T, ACC, ORD>(val + base, col + base, C, rl[p], cl[chunk], x, y,
+                                         order, p, n_rows, threadIdx.x & 31, pol_s, pol_x,
+                                         stage[threadIdx.x >> 5]);
+            }
             return;
         }
     }
@@ -924,7 +932,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         const char* e = getenv("SELLB_CARVEOUT");
         return e ? atoi(e) : -1;
     }();
-#define SELLB_LAUNCH(UU, LL, LR, NL, TH)                                                        \
+#define SELLB_LAUNCH(UU, LL, LR, NL, TH, SD)                                                    \
     do {                                                                                        \
         /* LONG instances run next to the row-group kernel: reserve shared */ \
         /* memory for one group CTA per SM up front (30 %), so an SM never */ \
@@ -955,11 +963,16 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
             cudaLaunchKernelEx(&cfg_, k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL>, m->cs, m->cl,  \
                                m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,  \
                                m->C, p0, p1, m->n_rows, (const int32_t*)(LR), (int64_t)(NL),   \
-                               (int)(TH), (const int32_t*)m->chunk_th, l2pol);                  \
+                               (int)(TH), (const int32_t*)m->chunk_th, l2pol,                   \
+                               (const int64_t*)((SD) ? m->side_off : nullptr),                  \
+                               (const int32_t*)((SD) ? m->side_col : nullptr),                  \
+                               (const T*)((SD) ? m->side_val : nullptr));                       \
         } else {                                                                                \
             k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(              \
                 m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
-                m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol);                       \
+                m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol,                        \
+                (SD) ? m->side_off : nullptr, (SD) ? m->side_col : nullptr,                     \
+                (const T*)((SD) ? m->side_val : nullptr));                                      \
         }                                                                                       \
         count_launches();                                                                       \
     } while (0)
@@ -1189,18 +1202,23 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         const int32_t* rest = rest_fused ? m->long_rest : nullptr;
         const int64_t n_rest = rest_fused ? m->n_rest : 0;
         grid += (unsigned)((n_rest + kThreads / 32 - 1) / (kThreads / 32));
-        if (u8) SELLB_LAUNCH(8, true, rest, n_rest, m->long_th);
-        else SELLB_LAUNCH(4, true, rest, n_rest, m->long_th);
+        const bool side = rest_fused && m->side_off;   // side table is indexed like long_rest
+        if (u8) SELLB_LAUNCH(8, true, rest, n_rest, m->long_th, side);
+        else SELLB_LAUNCH(4, true, rest, n_rest, m->long_th, side);
         if (long_mode == 2) SELLB_CU(cudaStreamWaitEvent(st, mm->ev_join, 0));
     } else if (n_long) {
-        if (u8) SELLB_LAUNCH(8, true, m->long_rows, n_long, m->long_th);
-        else SELLB_LAUNCH(4, true, m->long_rows, n_long, m->long_th);
+        // no row groups: long_rest holds every long row (same order), so the
+        // side table applies unless the fused warp-per-row role is forced
+        const bool side = long_mode != 0 && m->side_off && m->n_rest == n_long;
+        const int32_t* lr = side ? m->long_rest : m->long_rows;
+        if (u8) SELLB_LAUNCH(8, true, lr, n_long, m->long_th, side);
+        else SELLB_LAUNCH(4, true, lr, n_long, m->long_th, side);
     } else if (u_env == 6 || (!u_env && m->max_cl > 4 && m->max_cl <= 6 && sizeof(T) == 8)) {
         // every chunk fits one 6-slot batch (5-point stencils): one round trip
-        SELLB_LAUNCH(6, false, nullptr, 0, 0x7fffffff);
+        SELLB_LAUNCH(6, false, nullptr, 0, 0x7fffffff, false);
     } else {
-        if (u8) SELLB_LAUNCH(8, false, nullptr, 0, 0x7fffffff);
-        else SELLB_LAUNCH(4, false, nullptr, 0, 0x7fffffff);
+        if (u8) SELLB_LAUNCH(8, false, nullptr, 0, 0x7fffffff, false);
+        else SELLB_LAUNCH(4, false, nullptr, 0, 0x7fffffff, false);
     }
 #undef SELLB_LAUNCH
     return 0;
