@@ -20,6 +20,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <functional>
 #include <vector>
 
 #include "sellb_internal.cuh"
@@ -329,20 +330,45 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     int th = 256, th_hi = 512;      // th_hi 512/1024/2048 on cfg3 sigma=N: 742/674/426
     if (const char* e = getenv("SELLB_LONG_TH")) th = th_hi = atoi(e);
     if (const char* e = getenv("SELLB_LONG_TH_HI")) th_hi = atoi(e);
+    // Rule 1: a row is long when it is longer than th_hi, or than
+    // max(floor, f * the chunk's k-th longest row) -- i.e. it stands out of
+    // its own chunk (unsorted layouts: one or two long rows among short ones,
+    // whose slots would each cost a DRAM line in the bulk) and then reads
+    // from the side table; sorted chunks (k-th longest close to the longest)
+    // keep their rows in the coalesced bulk role.  Rule 0: the earlier
+    // min/max heterogeneity test with the fixed threshold th.
+    // Default: rule 1 for unsorted / shortly-sorted layouts (sigma_eff <=
+    // 4 C), rule 0 for long scopes whose chunks descend smoothly (measured on
+    // cfg3, tools/rule_ab.sh: sigma=1 246 -> 318 GF/s, sigma=128 441 -> 466
+    // with rule 1; sigma=512 590 vs 576 keeps rule 0; sigma=N and cfg4 equal).
+    const int rule = getenv("SELLB_LONG_RULE") ? atoi(getenv("SELLB_LONG_RULE"))
+                                               : (m->sigma_eff <= 4 * m->C ? 1 : 0);
+    const int floor_th = getenv("SELLB_LONG_FLOOR") ? atoi(getenv("SELLB_LONG_FLOOR")) : 64;
+    const int kth = std::max(1, getenv("SELLB_LONG_K") ? atoi(getenv("SELLB_LONG_K")) : 8);
+    const int fct = std::max(1, getenv("SELLB_LONG_F") ? atoi(getenv("SELLB_LONG_F")) : 2);
+    if (rule == 1 && !getenv("SELLB_LONG_TH")) th = std::min(th, floor_th);
     if (th <= 0 || m->max_cl <= th) return 0;
     std::vector<int32_t> h_rl(m->n_pad), h_cl(m->n_chunks);
     SELLB_CU(cudaMemcpyAsync(h_rl.data(), m->rl, m->n_pad * 4, cudaMemcpyDeviceToHost, st));
     SELLB_CU(cudaMemcpyAsync(h_cl.data(), m->cl, m->n_chunks * 4, cudaMemcpyDeviceToHost, st));
     SELLB_CU(cudaStreamSynchronize(st));
-    std::vector<int32_t> cth(m->n_chunks, th_hi), rows;
+    std::vector<int32_t> cth(m->n_chunks, th_hi), rows, lens(m->C);
     for (int64_t c = 0; c < m->n_chunks; ++c) {
         if (h_cl[c] <= th) continue;
-        int32_t lo = 0x7fffffff, hi = 0;
-        for (int64_t r = 0; r < m->C; ++r) {
-            lo = std::min(lo, h_rl[c * m->C + r]);
-            hi = std::max(hi, h_rl[c * m->C + r]);
+        if (rule == 1) {
+            for (int64_t r = 0; r < m->C; ++r) lens[r] = h_rl[c * m->C + r];
+            const int64_t k = std::min<int64_t>(kth, m->C) - 1;
+            std::nth_element(lens.begin(), lens.begin() + k, lens.end(), std::greater<int32_t>());
+            const int64_t t = std::max<int64_t>(th, (int64_t)fct * lens[k]);
+            cth[c] = (int32_t)std::min<int64_t>(th_hi, t);
+        } else {
+            int32_t lo = 0x7fffffff, hi = 0;
+            for (int64_t r = 0; r < m->C; ++r) {
+                lo = std::min(lo, h_rl[c * m->C + r]);
+                hi = std::max(hi, h_rl[c * m->C + r]);
+            }
+            if ((int64_t)lo * 4 < hi) cth[c] = th;
         }
-        if ((int64_t)lo * 4 < hi) cth[c] = th;
         for (int64_t r = 0; r < m->C; ++r)
             if (h_rl[c * m->C + r] > cth[c]) rows.push_back((int32_t)(c * m->C + r));
     }
