@@ -385,8 +385,20 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     // holding >= 4 long rows (sorted chunks of long rows), longest first
     std::vector<int32_t> groups, rest;
     std::vector<int32_t> gmax;
-    const bool use_groups = m->C % 8 == 0 && !(getenv("SELLB_LONG_GRP") &&
-                                                atoi(getenv("SELLB_LONG_GRP")) == 0);
+    // When every long row fits the side table (<= 1/4 of the nonzeros), all
+    // of them take the side-table warp-per-row role and no row groups are
+    // formed (tools/grp_vs_side.sh: cfg3 sigma=N 843 -> 882 GF/s, cfg4
+    // sigma=N C=32/128 733/735 -> 748/758, C=8 707 -> 697); larger long-row
+    // shares keep the row-group kernel.  SELLB_LONG_GRP=1 forces groups, =0
+    // disables them.
+    const bool want_side_all = !(getenv("SELLB_LONG_SIDE") && atoi(getenv("SELLB_LONG_SIDE")) == 0);
+    int64_t long_total = 0;
+    for (int32_t p : rows) long_total += h_rl[p];
+    const char* grp_env = getenv("SELLB_LONG_GRP");
+    const bool use_groups =
+        m->C % 8 == 0 &&
+        (grp_env ? atoi(grp_env) != 0
+                 : !(want_side_all && long_total * 4 <= std::max<int64_t>(m->nnz, 1)));
     if (use_groups) {
         std::vector<uint8_t> is_long(m->n_pad, 0);
         for (int32_t p : rows) is_long[p] = 1;

@@ -100,15 +100,19 @@ print("ok" if not bad else "fail")
 '''
 
 MODES = [
-    {"SELLB_LONG_MODE": "2"},                                  # default
+    {"SELLB_LONG_MODE": "2"},                                  # default (side table)
+    {"SELLB_LONG_MODE": "2", "SELLB_LONG_GRP": "1"},           # row groups forced
     {"SELLB_LONG_MODE": "0"},
     {"SELLB_LONG_MODE": "1"},
-    {"SELLB_LONG_MODE": "2", "SELLB_GRP_SB": "128"},
-    {"SELLB_LONG_MODE": "2", "SELLB_GRP_CTAS": "3", "SELLB_LONG_REST": "1"},
+    {"SELLB_LONG_MODE": "2", "SELLB_GRP_SB": "128", "SELLB_LONG_GRP": "1"},
+    {"SELLB_LONG_MODE": "2", "SELLB_GRP_CTAS": "3", "SELLB_LONG_REST": "1",
+     "SELLB_LONG_GRP": "1"},
     {"SELLB_LONG_MODE": "1", "SELLB_LONG_GRP": "0", "SELLB_LONG_REST": "1",
      "SELLB_LONG_D": "3"},
-    {"SELLB_LONG_MODE": "2", "SELLB_LONG_TMA": "0"},            # isolated rows fused
-    {"SELLB_LONG_MODE": "1", "SELLB_LONG_GRP": "0"},            # every long row by TMA
+    {"SELLB_LONG_MODE": "2", "SELLB_LONG_TMA": "0", "SELLB_LONG_SIDE": "0"},  # padded reads
+    {"SELLB_LONG_MODE": "2", "SELLB_LONG_SIDE": "0"},           # groups + fused, no side table
+    {"SELLB_LONG_MODE": "1", "SELLB_LONG_GRP": "0", "SELLB_LONG_TMA": "1",
+     "SELLB_LONG_SIDE": "0"},                                  # every long row by TMA
 ]
 
 
