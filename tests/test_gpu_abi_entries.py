@@ -110,3 +110,24 @@ def test_int64_offsets_beyond_2p31_slots():
     s.free()
     del xd
     torch.cuda.empty_cache()
+
+
+def test_launch_counter_counts_spmv_kernels():
+    """sellb_launch_count: one launch per plain SpMV, two for the L2 flush
+    (the bench's gpu_launches is built from it)."""
+    import torch
+    lib = _lib.load()
+    m = generate.stencil27(16)
+    s = sb.crs_to_sell(m, 32, 1)
+    x = torch.from_numpy(generate.rhs(m.n_cols)).cuda()
+    y = torch.zeros(s.n_rows_padded, dtype=torch.float64, device="cuda")
+    sb.spmv_sell(s, x, y)
+    a = lib.sellb_launch_count()
+    for _ in range(5):
+        sb.spmv_sell(s, x, y)
+    assert lib.sellb_launch_count() - a == 5
+    scratch = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    a = lib.sellb_launch_count()
+    _lib.check(lib.sellb_l2_flush(scratch.data_ptr(), scratch.numel(),
+                                  torch.cuda.current_stream().cuda_stream))
+    assert lib.sellb_launch_count() - a == 2
