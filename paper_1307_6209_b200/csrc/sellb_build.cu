@@ -343,7 +343,7 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     // with rule 1; sigma=512 590 vs 576 keeps rule 0; sigma=N and cfg4 equal).
     const int rule = getenv("SELLB_LONG_RULE") ? atoi(getenv("SELLB_LONG_RULE"))
                                                : (m->sigma_eff <= 4 * m->C ? 1 : 0);
-    const int floor_th = getenv("SELLB_LONG_FLOOR") ? atoi(getenv("SELLB_LONG_FLOOR")) : 64;
+    const int floor_th = getenv("SELLB_LONG_FLOOR") ? atoi(getenv("SELLB_LONG_FLOOR")) : 48;
     const int kth = std::max(1, getenv("SELLB_LONG_K") ? atoi(getenv("SELLB_LONG_K")) : 8);
     const int fct = std::max(1, getenv("SELLB_LONG_F") ? atoi(getenv("SELLB_LONG_F")) : 2);
     if (rule == 1 && !getenv("SELLB_LONG_TH")) th = std::min(th, floor_th);
