@@ -566,6 +566,7 @@ def run_ours(args):
         "config": {"workload": f"{desc}, SELL-{args.C}-{sigma}", "C": args.C, "sigma": sigma,
                    "n_rows": n_rows, "nnz": nnz, "slots": slots,
                    "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
+                   "long_rows": s.long_rows_info(),
                    "l2": ("flushed between steps (%d MB scratch write, then half of it "
                           "read back so the L2 holds clean lines); value from the SpMV's "
                           "own events" % (4 * l2_bytes // 2**20)) if flush is not None

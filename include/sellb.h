@@ -73,6 +73,13 @@ typedef struct sellb_info_t {
     int32_t max_cl;
 } sellb_info_t;
 
+/* How the matrix's long rows are handled (rows the bulk role skips):
+ * n_long rows in total, n_groups 8-row groups for the row-group kernel,
+ * n_rest rows for the warp-per-row role, side_entries of them copied to the
+ * contiguous side table (0 when the side table is off or too large). */
+int sellb_long_info(const sellb_mat* m, int64_t* n_long, int64_t* n_groups, int64_t* n_rest,
+                    int64_t* side_entries);
+
 /* raw device pointers of a matrix (borrowed; valid until sellb_free) */
 typedef struct sellb_dev_arrays_t {
     const int64_t* cs;

@@ -440,15 +440,18 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
         SELLB_CU(cudaMemcpyAsync(m->long_rest, rest.data(), rest.size() * 4,
                                  cudaMemcpyHostToDevice, st));
     }
-    // side table for the rest rows (bounded: at most a quarter of the
-    // matrix's entries)
+    // side table for the rest rows: at most one more copy of their entries
+    // (never more than the padded SELL arrays already hold), and only while
+    // it takes under a quarter of the free device memory
     const bool want_side = !(getenv("SELLB_LONG_SIDE") && atoi(getenv("SELLB_LONG_SIDE")) == 0);
     if (want_side && !rest.empty()) {
         std::vector<int64_t> off(rest.size() + 1, 0);
         for (size_t k = 0; k < rest.size(); ++k) off[k + 1] = off[k] + h_rl[rest[k]];
         const int64_t total = off.back();
-        if (total > 0 && total * 4 <= std::max<int64_t>(m->nnz, 1)) {
-            const size_t vs = vsize(m->dtype);
+        const size_t vs = vsize(m->dtype);
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+        if (total > 0 && (size_t)total * (vs + 4) + off.size() * 8 <= free_b / 4) {
             if (int rc = alloc_dev((void**)&m->side_off, off.size() * 8)) return rc;
             if (int rc = alloc_dev((void**)&m->side_col, total * 4)) return rc;
             if (int rc = alloc_dev(&m->side_val, total * vs)) return rc;
@@ -805,6 +808,24 @@ int sellb_info(const sellb_mat* m, sellb_info_t* info) {
     info->slots = m->slots; info->nnz = m->nnz; info->dtype = m->dtype; info->device = m->device;
     info->col_permuted = m->col_permuted; info->variant = m->variant;
     info->has_row_lengths = m->rl != nullptr; info->max_cl = m->max_cl;
+    return 0;
+}
+
+int sellb_long_info(const sellb_mat* m, int64_t* n_long, int64_t* n_groups, int64_t* n_rest,
+                    int64_t* side_entries) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    int64_t side = 0;
+    if (m->side_off && m->n_rest) {
+        int64_t last = 0;
+        if (cudaMemcpy(&last, m->side_off + m->n_rest, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return set_error(SELLB_ERESOURCE, "side-table offset read failed");
+        side = last;
+    }
+    if (n_long) *n_long = m->n_long;
+    if (n_groups) *n_groups = m->n_groups;
+    if (n_rest) *n_rest = m->n_rest;
+    if (side_entries) *side_entries = side;
     return 0;
 }
 

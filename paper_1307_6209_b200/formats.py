@@ -395,6 +395,15 @@ class SellMatrix:
         _lib.check(_lib.load().sellb_device_arrays(self.handle, ctypes.byref(d)))
         return {name: getattr(d, name) for name, _ in d._fields_}
 
+    def long_rows_info(self):
+        """How the long rows are handled: {"n_long", "n_groups", "n_rest",
+        "side_entries"} (sellb_long_info)."""
+        vals = [ctypes.c_int64() for _ in range(4)]
+        _lib.check(_lib.require_device().sellb_long_info(self.handle,
+                                                         *[ctypes.byref(v) for v in vals]))
+        return dict(zip(("n_long", "n_groups", "n_rest", "side_entries"),
+                        (v.value for v in vals)))
+
     def sector_occupancy(self):
         """(beta_eff, val_sectors, col_sectors): occupancy counted in the
         32-byte sectors the pad-skipping kernel touches."""

@@ -134,3 +134,20 @@ def test_group_structure_is_exercised():
     rl1 = sb.crs_to_sell(m, 32, 1).row_lengths               # unsorted: isolated rows
     g1 = [int((rl1[g:g + 8] > 256).sum()) for g in range(0, len(rl1), 8)]
     assert any(0 < c < 4 for c in g1)
+
+
+def test_long_rows_info_reports_the_paths():
+    """sellb_long_info: unsorted isolated long rows -> side table, no groups;
+    SELLB_LONG_GRP=1 -> row groups (child process: the knob is read at build)."""
+    m = long_mix(1)
+    info = sb.crs_to_sell(m, 32, 1).long_rows_info()
+    assert info["n_long"] > 0 and info["n_groups"] == 0
+    assert info["n_rest"] == info["n_long"] and info["side_entries"] > 0
+    code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+            "import paper_1307_6209_b200 as sb; from test_gpu_long_rows import long_mix;"
+            "m = long_mix(1); print(sb.crs_to_sell(m, 32, m.n_rows).long_rows_info())")
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SELLB_LONG_GRP="1"),
+                         capture_output=True, text=True, cwd=REPO, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = eval(out.stdout.strip().splitlines()[-1])
+    assert d["n_groups"] >= 9
