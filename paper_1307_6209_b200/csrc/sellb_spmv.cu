@@ -633,7 +633,15 @@ constexpr size_t grp_smem() {
 // long-row role (the same rule builds long_rows[], sellb_build.cu) and the
 // others stop at their own length (pad-skip semantics).
 template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U, bool LONG>
-__global__ void __launch_bounds__(kThreads, U == 4 ? (LONG ? 6 : 8) : (U == 6 ? 6 : 5))
+#ifndef SELLB_F64_BLOCKS
+#define SELLB_F64_BLOCKS 5
+#endif
+#ifndef SELLB_F32_BLOCKS
+#define SELLB_F32_BLOCKS 6   // fp32 U=8: 40 regs, 48 warps/SM (tools/f32occ_ab.sh: cfg4 f32 881 -> 1050)
+#endif
+__global__ void __launch_bounds__(kThreads, U == 4 ? (LONG ? 6 : 8)
+                                             : (U == 6 ? 6 : (sizeof(T) == 4 ? SELLB_F32_BLOCKS
+                                                                            : SELLB_F64_BLOCKS)))
 k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
