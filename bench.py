@@ -298,11 +298,9 @@ def model_block(s, nnz, n_rows, n_cols, n_pad, n_chunks, slots, s_v, traffic, ke
             a = model.infer_alpha(traffic, nnz, nnz / slots, nzr, line_bytes=32)
             out["alpha_paper"] = round(a.alpha, 4)
             out["alpha_ideal"] = round(1.0 / nzc, 4)
-            if s.variant == "pad_incl":
-                mat, extra = 12 * slots, 0
-            elif vs is not None:
-                mat, extra = 32 * (vs + cs_), 4 * n_pad
-            else:
+            try:                           # bytes the kernels stream as configured
+                mat, _, extra = s.streamed_bytes()
+            except Exception:
                 mat = None
             if mat is not None:
                 out["alpha_eff"] = round(model.alpha_from_traffic(

@@ -80,6 +80,15 @@ typedef struct sellb_info_t {
 int sellb_long_info(const sellb_mat* m, int64_t* n_long, int64_t* n_groups, int64_t* n_rest,
                     int64_t* side_entries);
 
+/* Bytes of val/col the SpMV streams for this matrix as configured (for the
+ * alpha-from-DRAM-bytes model, model.py alpha_from_traffic): every slot of
+ * pad-inclusive chunks, the 32-byte (and 64-byte) sectors of bulk rows in
+ * chunks read with pad-skip semantics, the long rows' entries (contiguous
+ * side table, or one sector per element from the padded layout);
+ * extra_bytes = the row_lengths reads. */
+int sellb_streamed_bytes(const sellb_mat* m, int64_t* matrix_bytes, int64_t* matrix_bytes_64,
+                         int64_t* extra_bytes, void* stream);
+
 /* raw device pointers of a matrix (borrowed; valid until sellb_free) */
 typedef struct sellb_dev_arrays_t {
     const int64_t* cs;

@@ -35,7 +35,7 @@ EXPORTED = (
     "sellb_pad_fixup", "sellb_gen_hamiltonian_rpt", "sellb_gen_hamiltonian_fill",
     "sellb_export_range", "sellb_infer_row_lengths", "sellb_chunk_flags",
     "sellb_coo_to_crs", "sellb_mm_parse_body", "sellb_mm_format_body",
-    "sellb_launch_count", "sellb_long_info",
+    "sellb_launch_count", "sellb_long_info", "sellb_streamed_bytes",
 )
 
 
@@ -106,6 +106,8 @@ _PROTOS = {
     "sellb_coo_to_crs": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
                                         ctypes.POINTER(_i64), _i32, _vp, _i32]),
     "sellb_launch_count": (_i64, []),
+    "sellb_streamed_bytes": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                            ctypes.POINTER(_i64), _vp]),
     "sellb_long_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                        ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sellb_mm_parse_body": (ctypes.c_int, [_vp, _i64, _i32, _i64, _vp, ctypes.POINTER(_i64),

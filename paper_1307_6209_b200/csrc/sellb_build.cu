@@ -163,6 +163,65 @@ __global__ void k_sector_count(const int32_t* __restrict__ rl, int64_t n_pad, in
     }
 }
 
+// Bytes of val/col the SpMV kernels stream for this matrix as configured:
+// pad-inclusive chunks (no long-row role in them) read every slot; chunks
+// read with pad-skip semantics read the 32-byte sectors holding an active
+// lane of a bulk row (long rows -- rl > chunk_th of a chunk wider than
+// long_th -- excluded: they go to the long-row roles) plus row_lengths.
+// One thread per chunk; gv / gc = lanes per val / col sector, g = 64-byte
+// granularity variant (2 sectors) for the DRAM-transfer estimate.
+__global__ void k_stream_count(const int32_t* __restrict__ rl, const int32_t* __restrict__ cl,
+                               const int32_t* __restrict__ chunk_th, int64_t n_chunks,
+                               int64_t C, int skip_variant, int long_th, int vs,
+                               unsigned long long* __restrict__ out /* [4] */) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long incl = 0, s32 = 0, s64 = 0, rlb = 0;
+    if (c < n_chunks) {
+        const int w = cl[c];
+        const bool longish = chunk_th && w > long_th;
+        if (!skip_variant && !longish) {
+            incl = (unsigned long long)C * w * (vs + 4);
+        } else {
+            const int th = longish ? chunk_th[c] : 0x7fffffff;
+            const int gv = 32 / vs, gc = 8;
+            for (int pass = 0; pass < 2; ++pass) {          // 32-byte, then 64-byte sectors
+                const int mul = pass ? 2 : 1;
+                unsigned long long acc = 0;
+                for (int64_t r0 = 0; r0 < C; r0 += gv * mul) {
+                    int mv = 0;
+                    for (int64_t r = r0; r < r0 + gv * mul && r < C; ++r) {
+                        const int l = rl[c * C + r];
+                        mv = max(mv, l > th ? 0 : l);
+                    }
+                    acc += (unsigned long long)mv * 32ull * mul;
+                }
+                for (int64_t r0 = 0; r0 < C; r0 += gc * mul) {
+                    int mc = 0;
+                    for (int64_t r = r0; r < r0 + gc * mul && r < C; ++r) {
+                        const int l = rl[c * C + r];
+                        mc = max(mc, l > th ? 0 : l);
+                    }
+                    acc += (unsigned long long)mc * 32ull * mul;
+                }
+                if (pass) s64 = acc; else s32 = acc;
+            }
+            rlb = 4ull * C;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        incl += __shfl_xor_sync(0xffffffffu, incl, o);
+        s32 += __shfl_xor_sync(0xffffffffu, s32, o);
+        s64 += __shfl_xor_sync(0xffffffffu, s64, o);
+        rlb += __shfl_xor_sync(0xffffffffu, rlb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, incl);
+        atomicAdd(out + 1, s32);
+        atomicAdd(out + 2, s64);
+        atomicAdd(out + 3, rlb);
+    }
+}
+
 // .sell cache semantics (io.py:308-321): length = chunk width minus the
 // trailing run of padding-looking slots (value 0.0 and column 0)
 template <typename T>
@@ -939,6 +998,46 @@ double sellb_chunk_occupancy(const sellb_mat* m) {
     // formats.py:274-282
     if (!m || m->slots == 0) return 1.0;
     return (double)m->nnz / (double)m->slots;
+}
+
+int sellb_streamed_bytes(const sellb_mat* m, int64_t* matrix_bytes, int64_t* matrix_bytes_64,
+                         int64_t* extra_bytes, void* stream) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    DeviceGuard guard(m->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int vs = (int)vsize(m->dtype);
+    unsigned long long h[4] = {0, 0, 0, 0};
+    const bool skip = m->variant == SELLB_VARIANT_PAD_SKIP;
+    if (m->n_chunks && (m->rl || !skip)) {
+        DBuf cnt;
+        SELLB_CU(cnt.alloc(sizeof(h), st));
+        SELLB_CU(cudaMemsetAsync(cnt.p, 0, sizeof(h), st));
+        if (m->rl) {
+            k_stream_count<<<(unsigned)grid_for(m->n_chunks, 256), 256, 0, st>>>(
+                m->rl, m->cl, m->chunk_th, m->n_chunks, m->C, skip ? 1 : 0, m->long_th, vs,
+                cnt.as<unsigned long long>());
+            SELLB_CU(cudaGetLastError());
+            SELLB_CU(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        } else {
+            h[0] = (unsigned long long)m->slots * (vs + 4);
+        }
+        SELLB_CU(cudaStreamSynchronize(st));
+    }
+    int64_t side = 0;
+    if (int rc = sellb_long_info(m, nullptr, nullptr, nullptr, &side)) return rc;
+    const int64_t long_bytes = side * (vs + 4);     // side-table rows read contiguously
+    int64_t long_direct = 0;                        // long rows read from the SELL arrays
+    if (!side && m->n_long && m->rl) {
+        std::vector<int32_t> lr(m->n_long), hrl(m->n_pad);
+        SELLB_CU(cudaMemcpy(lr.data(), m->long_rows, m->n_long * 4, cudaMemcpyDeviceToHost));
+        SELLB_CU(cudaMemcpy(hrl.data(), m->rl, m->n_pad * 4, cudaMemcpyDeviceToHost));
+        for (int32_t p : lr) long_direct += (int64_t)hrl[p] * 32 * 2;   // a sector per value / index
+    }
+    if (matrix_bytes) *matrix_bytes = (int64_t)(h[0] + h[1]) + long_bytes + long_direct;
+    if (matrix_bytes_64) *matrix_bytes_64 = (int64_t)(h[0] + h[2]) + long_bytes + 2 * long_direct;
+    if (extra_bytes) *extra_bytes = (int64_t)h[3];
+    return 0;
 }
 
 int sellb_sector_occupancy(const sellb_mat* m, double* beta_eff, int64_t* val_sectors,

@@ -395,6 +395,14 @@ class SellMatrix:
         _lib.check(_lib.load().sellb_device_arrays(self.handle, ctypes.byref(d)))
         return {name: getattr(d, name) for name, _ in d._fields_}
 
+    def streamed_bytes(self):
+        """(matrix bytes at 32-byte sectors, at 64-byte granularity, extra
+        row_lengths bytes) the SpMV streams as configured (sellb_streamed_bytes)."""
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.require_device().sellb_streamed_bytes(
+            self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), None))
+        return a.value, b.value, c.value
+
     def long_rows_info(self):
         """How the long rows are handled: {"n_long", "n_groups", "n_rest",
         "side_entries"} (sellb_long_info)."""

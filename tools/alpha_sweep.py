@@ -51,7 +51,10 @@ def run(out_json, timed=False):
         # 64-byte granularity (two sectors): 8 fp64 lanes of val, 16 of col
         v64 = int(rl.reshape(-1, 8).max(1).sum()) * 2
         c64 = int(rl.reshape(-1, 16).max(1).sum()) * 2
+        mb32, mb64, mx = s.streamed_bytes()
         rec = {"name": name, "sigma": sigma, "nnz": info.nnz, "n_rows": info.n_rows,
+               "stream32": mb32, "stream64": mb64, "stream_extra": mx,
+               "long_rows": s.long_rows_info(),
                "n_cols": info.n_cols, "n_pad": info.n_rows_padded, "n_chunks": info.n_chunks,
                "slots": info.slots, "beta": info.nnz / info.slots, "beta_eff": be,
                "val_sectors": vs, "col_sectors": cs, "val_sectors64": v64,
@@ -94,8 +97,9 @@ def report(layouts_json, ncu_csv, times_json):
     print("# sigma sweep with measured alpha (one B200)\n")
     print("alpha_paper = `infer_alpha(dram, nnz, beta, N_nzr, line=32)` (model.py:124-142 "
           "with B200's 32 B sector as the line); alpha_eff = `alpha_from_traffic` with the "
-          "bytes the kernel variant actually streams (all slots for pad-incl, touched sectors "
-          "+ row_lengths for pad-skip).  Ideal alpha = 1/N_nzc.  DRAM = ncu "
+          "bytes the kernels actually stream as configured (`sellb_streamed_bytes`: all slots "
+          "of pad-incl chunks, touched 32 B / 64 B sectors of bulk rows + row_lengths for "
+          "pad-skip chunks, long rows from the contiguous side table).  Ideal alpha = 1/N_nzc.  DRAM = ncu "
           "dram__bytes_read.sum + dram__bytes_write.sum of one cold SpMV launch; "
           "GF/s from CUDA events (50 warm launches).\n")
     print("| matrix | sigma | beta | beta_eff | variant | DRAM MB | V_alg MB | matrix MB (32 B / 64 B) | "
@@ -110,13 +114,9 @@ def report(layouts_json, ncu_csv, times_json):
         nnz, n = row["nnz"], row["n_rows"]
         nzr, nzc = nnz / n, nnz / row["n_cols"]
         a_p = model.infer_alpha(dram, nnz, row["beta"], nzr, line_bytes=32)
-        if row["variant"] == "pad_incl":
-            mat = mat64 = 12 * row["slots"]
-            extra = 0
-        else:
-            mat = 32 * (row["val_sectors"] + row["col_sectors"])
-            mat64 = 32 * (row["val_sectors64"] + row["col_sectors64"])
-            extra = 4 * row["n_pad"]
+        # what the kernels stream as configured (sellb_streamed_bytes: bulk
+        # sectors, long rows from the side table, row_lengths)
+        mat, mat64, extra = row["stream32"], row["stream64"], row["stream_extra"]
         a_e = model.alpha_from_traffic(dram, nnz, mat, row["n_pad"], row["n_chunks"],
                                        extra_bytes=extra)
         a_64 = model.alpha_from_traffic(dram, nnz, mat64, row["n_pad"], row["n_chunks"],
