@@ -19,6 +19,7 @@
  *   sellb_spmv_crs_range_host   kernels-module protocol    _kernels.pyx:17-31
  *   sellb_spmv_crs_unrolled_range_host                     _kernels.pyx:34-62
  *   sellb_read_sum / sellb_copy  membench kernels           _kernels.pyx:142-170
+ *   sellb_lru_stream_misses   kernels-module protocol    _kernels.pyx:95-139 (cachesim.py:74)
  *   sellb_chunk_occupancy     chunk_occupancy              formats.py:274-282
  *
  * Threading: every entry point is safe to call concurrently from several
@@ -265,6 +266,24 @@ int sellb_mm_format_body(const int64_t* rows, const int64_t* cols, const double*
  * long-row kernels, halo gather/scatter, pad fix-up, CRS kernels, L2 flush,
  * membench kernels): the bench's gpu_launches is a difference of two reads. */
 int64_t sellb_launch_count(void);
+
+/* lru_stream_misses (_kernels.pyx:95-139): misses of a fully-associative LRU
+ * cache of cache_lines lines replaying lines[0..n) (ids in [0, n_line_slots)),
+ * the RHS-traffic simulator behind cachesim.simulate_rhs_traffic.  Computed
+ * on the device from LRU stack distances (sellb_lru.cu); n == 0 -> 0,
+ * cache_lines <= 0 -> n as in the reference; an id outside the table ->
+ * SELLB_EPARAM.  lines may be host (lines_on_device = 0) or device memory. */
+int sellb_lru_stream_misses(const int64_t* lines, int64_t n, int64_t cache_lines,
+                            int64_t n_line_slots, int32_t lines_on_device,
+                            int64_t* misses, void* stream);
+
+/* The x line ids (col / elems_per_line, elems_per_line a power of two) of
+ * the matrix's real entries in kernel traversal order -- chunk by chunk,
+ * slot-major then lane, padding dropped (cachesim.py:31-46) -- written to
+ * the device buffer lines[nnz]; *n_out = nnz.  Feeds
+ * sellb_lru_stream_misses(lines_on_device = 1) without a host pass. */
+int sellb_sell_x_lines(const sellb_mat* m, int32_t elems_per_line, int64_t* lines,
+                       int64_t* n_out, void* stream);
 
 /* Pinned host buffers for the end-to-end path. */
 int sellb_host_alloc(size_t bytes, void** out);

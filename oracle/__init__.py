@@ -82,6 +82,8 @@ def lib():
         L.oracle_coo_to_crs.restype = _i64
         L.oracle_coo_to_crs.argtypes = [_i64p, _i64p, _f64p, _i64, _i64, _i64p, _i32p,
                                         _f64p]
+        L.oracle_lru_stream_misses.restype = _i64
+        L.oracle_lru_stream_misses.argtypes = [_i64p, _i64, _i64, _i64]
         _lib = L
     return _lib
 
@@ -231,6 +233,16 @@ def read_sum(a):
     """_kernels.pyx:142-161."""
     a = np.ascontiguousarray(a, dtype=np.float64)
     return float(lib().oracle_read_sum(_p(a, _f64p), len(a)))
+
+
+def lru_stream_misses(lines, cache_lines, n_line_slots):
+    """_kernels.pyx:95-139: misses of a fully-associative LRU cache."""
+    lines = np.ascontiguousarray(lines, dtype=np.int64)
+    r = lib().oracle_lru_stream_misses(_p(lines, _i64p), len(lines), int(cache_lines),
+                                       int(n_line_slots))
+    if r < 0:
+        raise MemoryError("oracle LRU table")
+    return int(r)
 
 
 def unpermute(v, perm):

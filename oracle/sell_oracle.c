@@ -384,3 +384,50 @@ int64_t oracle_coo_to_crs(const int64_t *rows, const int64_t *cols, const double
     free(ord); free(tmp);
     return u;
 }
+
+/* ---------------------------------------------------------------------- */
+/* LRU replay of a line-id stream: _kernels.pyx:95-139 (cachesim.py:74)    */
+/* ---------------------------------------------------------------------- */
+
+/* Fully-associative LRU cache of cache_lines lines, replayed access by
+ * access with an intrusive doubly-linked recency list over the dense id
+ * table (two sentinels after the n_slots ids).  Returns the miss count, or
+ * -1 when memory runs out. */
+int64_t oracle_lru_stream_misses(const int64_t *lines, int64_t n, int64_t cache_lines,
+                                 int64_t n_slots)
+{
+    if (n == 0) return 0;
+    if (cache_lines <= 0) return n;
+    const int64_t mru = n_slots, lru = n_slots + 1;       /* sentinels */
+    int64_t *fwd = malloc((size_t)(n_slots + 2) * sizeof(int64_t));   /* toward LRU */
+    int64_t *bwd = malloc((size_t)(n_slots + 2) * sizeof(int64_t));   /* toward MRU */
+    unsigned char *in = calloc((size_t)(n_slots ? n_slots : 1), 1);
+    if (!fwd || !bwd || !in) { free(fwd); free(bwd); free(in); return -1; }
+    fwd[mru] = lru;
+    bwd[lru] = mru;
+    int64_t misses = 0, held = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t l = lines[k];
+        if (in[l]) {                       /* hit: detach, re-attach at MRU */
+            fwd[bwd[l]] = fwd[l];
+            bwd[fwd[l]] = bwd[l];
+        } else {
+            ++misses;
+            if (held == cache_lines) {     /* evict the least recent line */
+                const int64_t v = bwd[lru];
+                fwd[bwd[v]] = lru;
+                bwd[lru] = bwd[v];
+                in[v] = 0;
+            } else {
+                ++held;
+            }
+            in[l] = 1;
+        }
+        fwd[l] = fwd[mru];
+        bwd[fwd[mru]] = l;
+        bwd[l] = mru;
+        fwd[mru] = l;
+    }
+    free(fwd); free(bwd); free(in);
+    return misses;
+}

@@ -36,6 +36,7 @@ EXPORTED = (
     "sellb_export_range", "sellb_infer_row_lengths", "sellb_chunk_flags",
     "sellb_coo_to_crs", "sellb_mm_parse_body", "sellb_mm_format_body",
     "sellb_launch_count", "sellb_long_info", "sellb_streamed_bytes",
+    "sellb_lru_stream_misses", "sellb_sell_x_lines",
 )
 
 
@@ -106,6 +107,8 @@ _PROTOS = {
     "sellb_coo_to_crs": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
                                         ctypes.POINTER(_i64), _i32, _vp, _i32]),
     "sellb_launch_count": (_i64, []),
+    "sellb_lru_stream_misses": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i32, _vp, _vp]),
+    "sellb_sell_x_lines": (ctypes.c_int, [_vp, _i32, _vp, ctypes.POINTER(_i64), _vp]),
     "sellb_streamed_bytes": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                             ctypes.POINTER(_i64), _vp]),
     "sellb_long_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64),

@@ -13,8 +13,8 @@ reference's test fixture (tests/conftest.py:38-43).
     spmv_crs_unrolled_range   _kernels.pyx:34-62   (bitwise equal)
     read_sum                  _kernels.pyx:142-161 (device reduction; rounding differs)
     copy_array                _kernels.pyx:164-170
-    lru_stream_misses         not provided: on B200 alpha is measured from
-                              DRAM counters (ncu) instead of simulated
+    lru_stream_misses         _kernels.pyx:95-139  (LRU stack distances on the
+                              device, equal miss counts)
 
 Arrays are host NumPy buffers, as in the reference.  Matrix arrays are
 uploaded once and cached by buffer identity (containers are immutable,
@@ -151,7 +151,38 @@ def copy_array(src, dst):
 
 
 def lru_stream_misses(lines, cache_lines, n_line_slots):
-    raise ResourceError(
-        "lru_stream_misses is not provided by the cuda backend: on B200 the "
-        "RHS traffic factor alpha is measured from DRAM byte counters "
-        "(paper_1307_6209_b200.model.alpha_from_traffic)")
+    """_kernels.pyx:95-139: misses of a fully-associative LRU cache of
+    ``cache_lines`` lines replaying the line-id stream, counted on the GPU
+    from LRU stack distances (csrc/sellb_lru.cu).  Same result as the
+    reference's MRU-list walk; 0 for an empty stream, len(lines) for
+    cache_lines <= 0; an id outside [0, n_line_slots) is a ParameterError
+    (the reference indexes its table unchecked)."""
+    import ctypes
+    import torch
+    lib = _lib.require_device()
+    lines = np.ascontiguousarray(lines, dtype=np.int64)
+    out = ctypes.c_int64(0)
+    _lib.check(lib.sellb_lru_stream_misses(
+        lines.ctypes.data if len(lines) else None, len(lines), int(cache_lines),
+        int(n_line_slots), 0, ctypes.byref(out),
+        torch.cuda.current_stream().cuda_stream))
+    return int(out.value)
+
+
+def sell_rhs_misses(m, line_bytes, cache_lines, n_line_slots):
+    """LRU misses of a device-resident SellMatrix's x stream without a host
+    pass: the line ids are extracted on the device (sellb_sell_x_lines) and
+    replayed there (sellb_lru_stream_misses)."""
+    import ctypes
+    import torch
+    lib = _lib.require_device()
+    st = torch.cuda.current_stream(m.device).cuda_stream
+    with torch.cuda.device(m.device):
+        lines = torch.empty(max(m.nnz, 1), dtype=torch.int64, device=f"cuda:{m.device}")
+        n = ctypes.c_int64(0)
+        _lib.check(lib.sellb_sell_x_lines(m.handle, line_bytes // 8, lines.data_ptr(),
+                                          ctypes.byref(n), st))
+        out = ctypes.c_int64(0)
+        _lib.check(lib.sellb_lru_stream_misses(lines.data_ptr(), n.value, int(cache_lines),
+                                               int(n_line_slots), 1, ctypes.byref(out), st))
+    return int(out.value)

@@ -374,8 +374,74 @@ def make_mm_fixtures(out_dir):
     np.savez_compressed(os.path.join(out_dir, "mm_write.npz"), **outs)
 
 
+def lru_streams():
+    """Line-id streams for the LRU replay (_kernels.pyx:95-139): uniform
+    random ids, a cyclic sweep one line larger than some caches (LRU's worst
+    case), local reuse with far jumps (many reuse distances just around the
+    cache size, exercising the tiled stack-distance path), a single line."""
+    rng = np.random.default_rng(95)
+    out = {}
+    out["uniform"] = (rng.integers(0, 3000, 60000), 3000)
+    out["cyclic"] = (np.tile(np.arange(513), 40), 513)
+    base = np.repeat(np.arange(0, 20000, 7), 3) % 2600
+    jumps = rng.integers(0, 2600, len(base))
+    pick = rng.random(len(base)) < 0.3
+    out["local_far"] = (np.where(pick, jumps, base), 2600)
+    out["single"] = (np.zeros(5000, np.int64), 1)
+    out["sparse_ids"] = (rng.integers(0, 40, 9000) * 997, 40 * 997)
+    return out
+
+
+LRU_CACHES = (0, 1, 2, 31, 64, 255, 512, 513, 700, 1500, 2599, 2600, 2999, 3000, 5000)
+
+
+def make_lru_fixtures(out_dir):
+    """Miss counts of the reference's compiled lru_stream_misses and the
+    totals of its simulate_rhs_traffic (cachesim.py:49-75) on SELL and CRS
+    matrices."""
+    comp = load_ref_compiled()
+    from sellkit import simulate_rhs_traffic
+    arrays = {}
+    for name, (lines, slots) in lru_streams().items():
+        lines = np.ascontiguousarray(lines, np.int64)
+        arrays[f"{name}_lines"] = lines
+        arrays[f"{name}_slots"] = np.int64(slots)
+        arrays[f"{name}_misses"] = np.array(
+            [comp.lru_stream_misses(lines, c, slots) for c in LRU_CACHES], np.int64)
+    arrays["caches"] = np.array(LRU_CACHES, np.int64)
+    rng = np.random.default_rng(74)
+    traffic = []   # (case, C, sigma, cache_bytes, line_bytes, traffic)
+    kern = comp
+    mats = {0: coo_to_crs(random_coo(rng, 300, 300, 4000)),
+            1: coo_to_crs(gen_skewed(700, 4, 120, 9, seed=3)),
+            2: coo_to_crs(random_coo(rng, 150, 900, 3000))}
+    import sellkit.backend as be
+    old = be.kernels
+    be.kernels = kern
+    try:
+        for mi, m in mats.items():
+            arrays[f"mat{mi}_rpt"] = m.rpt
+            arrays[f"mat{mi}_col"] = m.col
+            arrays[f"mat{mi}_val"] = m.val
+            arrays[f"mat{mi}_shape"] = np.array([m.n_rows, m.n_cols], np.int64)
+            for C, sigma in ((0, 0), (1, 1), (4, 1), (8, 32), (32, 1), (32, 10 ** 9)):
+                obj = m if C == 0 else crs_to_sell(m, C, sigma)
+                for cache in (0, 64, 512, 4096, 1 << 20):
+                    for line in (8, 32, 64, 128):
+                        if cache % line:
+                            continue
+                        v = simulate_rhs_traffic(obj, cache, line, kernels=kern)
+                        traffic.append((mi, C, sigma, cache, line, v))
+    finally:
+        be.kernels = old
+    arrays["traffic"] = np.array(traffic, np.int64)
+    np.savez_compressed(os.path.join(out_dir, "lru.npz"), **arrays)
+
+
 if __name__ == "__main__":
-    if "--coo-only" in sys.argv:
+    if "--lru-only" in sys.argv:
+        make_lru_fixtures(HERE)
+    elif "--coo-only" in sys.argv:
         make_coo_fixtures(HERE)
     elif "--mm-only" in sys.argv:
         make_mm_fixtures(HERE)
@@ -383,3 +449,4 @@ if __name__ == "__main__":
         main()
         make_coo_fixtures(HERE)
         make_mm_fixtures(HERE)
+        make_lru_fixtures(HERE)

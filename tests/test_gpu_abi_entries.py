@@ -76,11 +76,6 @@ def test_membench_kernels():
     assert r.gbps > 1000 and c.gbps > 1000
 
 
-def test_lru_not_provided():
-    with pytest.raises(sb.ResourceError):
-        kernels_cuda.lru_stream_misses(np.zeros(3, np.int64), 2, 4)
-
-
 def test_int64_offsets_beyond_2p31_slots():
     """2^27-row cfg5-style matrix: > 2^31 stored slots (int64 cs and flat
     offsets end to end); sampled blocks bit-exact against the oracle."""
