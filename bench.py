@@ -306,6 +306,18 @@ def model_block(s, nnz, n_rows, n_cols, n_pad, n_chunks, slots, s_v, traffic, ke
                 out["alpha_eff"] = round(model.alpha_from_traffic(
                     traffic, nnz, mat, n_pad, n_chunks, extra_bytes=extra).alpha, 4)
             out["traffic_source"] = "profiles/ncu_traffic.json (ncu dram bytes, one launch)"
+        if s_v == 8 and nnz <= 200_000_000 and hasattr(s, "handle"):
+            # the reference's LRU model (cachesim.py:49-75) with an L2-sized
+            # fully-associative cache of 32 B lines, replayed on the device
+            try:
+                import torch
+                from paper_1307_6209_b200 import cachesim
+                l2 = (torch.cuda.get_device_properties(0).L2_cache_size // 32) * 32
+                v_sim = cachesim.simulate_rhs_traffic(s, l2, 32)
+                out["alpha_sim_lru_l2"] = round(
+                    model.infer_alpha(v_sim, nnz, nnz / slots, nzr, line_bytes=32).alpha, 4)
+            except Exception as e:         # reported, never fatal for the bench line
+                out["alpha_sim_lru_l2"] = f"unavailable: {type(e).__name__}"
     return out
 
 
