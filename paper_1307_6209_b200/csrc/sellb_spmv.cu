@@ -653,11 +653,13 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     const int64_t C = CC > 0 ? (int64_t)CC : C_rt;
     const uint64_t pol_s = make_policy(l2pol & 0xf);
     const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
-    const int64_t n_long_blocks = LONG ? (n_long + (kThreads / 32) - 1) / (kThreads / 32) : 0;
+    // block size: kThreads, or fewer (SELLB_BULK_BT) -- index math uses blockDim
+    const int64_t wpb = blockDim.x >> 5;
+    const int64_t n_long_blocks = LONG ? (n_long + wpb - 1) / wpb : 0;
     if constexpr (LONG) {
         if ((int64_t)blockIdx.x < n_long_blocks) {
             __shared__ T stage[kThreads / 32][kSeg * 32];
-            const int64_t k = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+            const int64_t k = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
             if (k >= n_long) return;
             const int64_t p = long_rows[k];
             if (p < p0 || p >= p1) return;
@@ -676,7 +678,8 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             return;
         }
     }
-    const int64_t p = p0 + ((int64_t)blockIdx.x - n_long_blocks) * kThreads + threadIdx.x;
+    const int64_t p = p0 + ((int64_t)blockIdx.x - n_long_blocks) * (int64_t)blockDim.x +
+                      threadIdx.x;
     if (p >= p1) return;
     const int64_t chunk = p / C;
     const int64_t base = cs[chunk] + (p - chunk * C);
@@ -903,8 +906,15 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     const int64_t rows = p1 - p0;
     if (rows <= 0) return 0;
     const int64_t n_long = m->long_rows ? m->n_long : 0;
-    const int64_t long_blocks = (n_long + kThreads / 32 - 1) / (kThreads / 32);
-    unsigned grid = (unsigned)(grid_for(rows, kThreads) + long_blocks);
+    // bulk block size (SELLB_BULK_BT = 64 / 128 / 256, A/B knob)
+    static const int bt_env = [] {
+        const char* e = getenv("SELLB_BULK_BT");
+        const int v = e ? atoi(e) : 0;
+        return (v == 64 || v == 128 || v == 256) ? v : 0;
+    }();
+    const int bt = bt_env ? bt_env : kThreads;
+    const int64_t long_blocks = (n_long + bt / 32 - 1) / (bt / 32);
+    unsigned grid = (unsigned)(grid_for(rows, bt) + long_blocks);
     // L2 policies: matrix streams (low nibble) and x gathers (high nibble);
     // 0 evict_first, 1 evict_normal, 2 evict_last.  x is always evict_last;
     // the matrix stream is evict_first while x fits comfortably in L2 and
@@ -961,7 +971,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         if (persist) {                                                                          \
             cudaLaunchConfig_t cfg_{};                                                          \
             cfg_.gridDim = dim3(grid);                                                          \
-            cfg_.blockDim = dim3(kThreads);                                                     \
+            cfg_.blockDim = dim3(bt);                                                           \
             cfg_.stream = st;                                                                   \
             cudaLaunchAttribute at_[1];                                                         \
             at_[0].id = cudaLaunchAttributeAccessPolicyWindow;                                  \
@@ -976,7 +986,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
                                (const int32_t*)((SD) ? m->side_col : nullptr),                  \
                                (const T*)((SD) ? m->side_val : nullptr));                       \
         } else {                                                                                \
-            k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, kThreads, 0, st>>>(              \
+            k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, bt, 0, st>>>(                    \
                 m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
                 m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol,                        \
                 (SD) ? m->side_off : nullptr, (SD) ? m->side_col : nullptr,                     \
@@ -1205,11 +1215,11 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         SELLB_CU(cudaGetLastError());
         // the bulk: rows above their chunk's threshold are skipped (LONG
         // template), no long-role blocks
-        grid = (unsigned)grid_for(rows, kThreads);
+        grid = (unsigned)grid_for(rows, bt);
         if (long_mode == 2) SELLB_CU(cudaEventRecord(mm->ev_join, ls));
         const int32_t* rest = rest_fused ? m->long_rest : nullptr;
         const int64_t n_rest = rest_fused ? m->n_rest : 0;
-        grid += (unsigned)((n_rest + kThreads / 32 - 1) / (kThreads / 32));
+        grid += (unsigned)((n_rest + bt / 32 - 1) / (bt / 32));
         const bool side = rest_fused && m->side_off;   // side table is indexed like long_rest
         if (u8) SELLB_LAUNCH(8, true, rest, n_rest, m->long_th, side);
         else SELLB_LAUNCH(4, true, rest, n_rest, m->long_th, side);
