@@ -617,7 +617,9 @@ def main(argv=None):
     ap.add_argument("--skip-parity", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--n", type=int, default=0, help="cfg5 rows (default 2^26)")
+    # --rows: under torchrun a bare --n is an ambiguous prefix of its own options
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=0,
+                    help="cfg5 rows (default 2^26)")
     args = ap.parse_args(argv)
     if args.sigma is None:
         args.sigma = 512 if args.config == "cfg5" else 1

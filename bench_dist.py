@@ -29,6 +29,11 @@ def bench_main(args):
                                            setup_device)
     from paper_1307_6209_b200.model import algorithmic_bytes
 
+    # NCCL prints its version banner on fd 1 at communicator creation; the
+    # driver reads exactly one JSON line from stdout, so everything but that
+    # line goes to stderr
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -170,6 +175,8 @@ def bench_main(args):
             "clocks": clk,
             "gpu_launches": int(launches),
         }
-        print(json.dumps(line), flush=True)
+        import sys
+        sys.stdout.flush()
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     tdist.destroy_process_group()
     return 0

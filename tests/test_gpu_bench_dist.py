@@ -1,0 +1,41 @@
+"""The N>1 leg of bench.py (bench_dist.py) launched the way the driver
+launches it -- torchrun, NCCL, one process per GPU -- at world size 1 on the
+one GPU this box has (SELLB_FORCE_DIST routes world 1 through the same code).
+Checks the stdout contract: exactly one JSON line, even though NCCL prints
+its version banner on fd 1 at communicator creation."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("extra", [["--config", "cfg5", "--rows", str(1 << 21)], []],
+                         ids=["cfg5_small", "cfg2"])
+def test_bench_dist_one_rank_stdout_is_one_json_line(extra):
+    env = dict(os.environ, SELLB_FORCE_DIST="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           "bench.py", "--gpus", "1", "--steps", "20", "--warmup", "3"] + extra
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 1 and rec["steps"] == 20 and rec["warmup"] == 3
+    assert rec["config"]["parity_vs_oracle_all_ranks"] is True
+    assert rec["value"] > 0 and rec["gpu_launches"] >= 20
+    assert rec["config"]["parallelism"] == "row-blocks x1"
