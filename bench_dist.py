@@ -94,6 +94,14 @@ def bench_main(args):
     for _ in range(args.warmup):
         ds.step()
     torch.cuda.synchronize()
+    # one CUDA graph per step (NCCL post included) unless SELLB_DIST_GRAPH=0;
+    # kept only if its replay is bitwise equal to the eager step on all ranks
+    graphed = False
+    if os.environ.get("SELLB_DIST_GRAPH", "1") != "0":
+        graphed = ds.capture()
+        for _ in range(args.warmup):
+            ds.step()
+        torch.cuda.synchronize()
     tdist.barrier()
     st = torch.cuda.current_stream(device)
     e0 = torch.cuda.Event(enable_timing=True)
@@ -120,6 +128,8 @@ def bench_main(args):
     par_t = torch.tensor([1.0 if parity in (True, None) else 0.0], device=device)
     tdist.all_reduce(par_t, op=tdist.ReduceOp.MIN)
     launches = ds.engine.lib.sellb_launch_count() - launches0
+    if graphed:   # replays do not pass through the library's launch counter
+        launches += ds.graph_launches * args.steps
 
     # e2e through host buffers: each rank's x slice H2D from pinned memory,
     # the distributed product, y slice D2H into pinned memory, every step
@@ -160,6 +170,7 @@ def bench_main(args):
                        "interior_ranges": len(ds.interior),
                        "boundary_ranges": len(ds.boundary), "build_s": round(build_s, 3),
                        "parity_vs_oracle_all_ranks": bool(par_t.item() == 1.0),
+                       "step_graph": graphed,
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": round(v_alg / (per_step_ms / 1e3) / 1e9, 2),
                          "peak": args.peak, "unit": "GB/s",
@@ -178,5 +189,7 @@ def bench_main(args):
         import sys
         sys.stdout.flush()
         os.write(json_fd, (json.dumps(line) + "\n").encode())
+    ds.release()
+    torch.cuda.synchronize()
     tdist.destroy_process_group()
     return 0

@@ -279,8 +279,75 @@ class DistSpmv:
             ops.append(tdist.P2POp(tdist.irecv, self.x0_buf, 0, group=self.group))
         return tdist.batch_isend_irecv(ops) if ops else []
 
+    graph = None
+    graph_launches = 0      # library kernels recorded in the graph (one step)
+
     def step(self):
         """y_local = A_local x (x_local must hold this rank's x slice)."""
+        if self.graph is not None:
+            self.graph.replay()
+            return self.y
+        return self._step_eager()
+
+    def capture(self):
+        """Record one step -- exchange post, interior, wait, boundary, x[0]
+        fix-up -- in a CUDA graph so later steps cost one replay of host
+        time instead of ~40-90 us of NCCL post per step
+        (profiles/r01f_p2p_overhead.txt).  Collective: every rank must call
+        it.  The graph is kept only if its replay reproduces the eager y
+        bitwise on EVERY rank (MIN-reduced flag); otherwise all ranks stay
+        eager.  Returns whether the graph is in use."""
+        if self.device.type != "cuda":
+            return False
+        def all_ok(v):
+            flag = torch.tensor([v], dtype=torch.float32, device=self.device)
+            tdist.all_reduce(flag, op=tdist.ReduceOp.MIN, group=self.group)
+            return float(flag.item()) == 1.0
+
+        g, y_ref, ok = None, None, 1.0
+        try:
+            self._step_eager()              # communicators exist before capture
+            torch.cuda.synchronize(self.device)
+            y_ref = self.y.clone()
+            g = torch.cuda.CUDAGraph()
+            l0 = self.engine.lib.sellb_launch_count()
+            # thread_local: the NCCL watchdog thread may query events meanwhile
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self._step_eager()
+            self.graph_launches = int(self.engine.lib.sellb_launch_count() - l0)
+        except Exception:                   # capture unsupported here: stay eager
+            ok = 0.0
+        # replay only when EVERY rank captured: a replayed NCCL send/recv whose
+        # peer does not replay would wait forever
+        if all_ok(ok):
+            ok = 1.0
+            try:
+                self.y.zero_()
+                g.replay()
+                torch.cuda.synchronize(self.device)
+                iv = torch.int64 if self.y.element_size() == 8 else torch.int32
+                ok = 1.0 if bool(torch.equal(self.y.view(iv), y_ref.view(iv))) else 0.0
+            except Exception:
+                ok = 0.0
+        else:
+            ok = 0.0
+        flag = torch.tensor([ok], dtype=torch.float32, device=self.device)
+        tdist.all_reduce(flag, op=tdist.ReduceOp.MIN, group=self.group)
+        self.graph = g if float(flag.item()) == 1.0 else None
+        if self.graph is None:
+            self._step_eager()              # leave y as an eager step made it
+            torch.cuda.synchronize(self.device)
+        return self.graph is not None
+
+    def release(self):
+        """Drop the step graph.  Call before destroy_process_group(): with
+        NCCL kernels captured, the teardown hangs while the graph is alive
+        (tools/p2p_graph_probe.py)."""
+        if self.graph is not None:
+            torch.cuda.synchronize(self.device)
+            self.graph = None
+
+    def _step_eager(self):
         works = self._post_exchange()
         self.engine.run_ranges(self.interior, self.x_full, self.y)
         for w in works:

@@ -39,3 +39,14 @@ def test_bench_dist_one_rank_stdout_is_one_json_line(extra):
     assert rec["config"]["parity_vs_oracle_all_ranks"] is True
     assert rec["value"] > 0 and rec["gpu_launches"] >= 20
     assert rec["config"]["parallelism"] == "row-blocks x1"
+    assert rec["config"]["step_graph"] is True
+
+
+def test_nccl_p2p_exchange_replays_from_a_cuda_graph():
+    """The mechanics DistSpmv.capture relies on: batch_isend_irecv + wait +
+    a consumer kernel captured once, replayed with new data."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           "tools/p2p_graph_probe.py"]
+    out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert out.returncode == 0 and "graph p2p ok" in out.stdout, out.stderr[-3000:]
