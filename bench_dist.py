@@ -94,12 +94,11 @@ def bench_main(args):
     for _ in range(args.warmup):
         ds.step()
     torch.cuda.synchronize()
-    # SELLB_DIST_GRAPH=1: one CUDA graph per step (NCCL post included), kept
-    # only if its replay is bitwise equal to the eager step on all ranks.
-    # Off by default: the one-GPU self-exchange test of a captured step with
-    # NCCL kernels inside (tools/dist_graph_selftest.py) hung this round
+    # one CUDA graph per step (NCCL post included) unless SELLB_DIST_GRAPH=0;
+    # kept only if its replay is bitwise equal to the eager step on all ranks
+    # (tools/dist_graph_selftest.py: NCCL P2P kernels inside the graph)
     graphed = False
-    if os.environ.get("SELLB_DIST_GRAPH", "0") == "1":
+    if os.environ.get("SELLB_DIST_GRAPH", "1") != "0":
         graphed = ds.capture()
         for _ in range(args.warmup):
             ds.step()

@@ -26,6 +26,8 @@ same code over gloo with a checker engine built on the oracle.
 """
 
 import math
+import os
+import sys
 
 import numpy as np
 
@@ -304,18 +306,25 @@ class DistSpmv:
             tdist.all_reduce(flag, op=tdist.ReduceOp.MIN, group=self.group)
             return float(flag.item()) == 1.0
 
+        def dbg(msg):
+            if os.environ.get("SELLB_DIST_DEBUG"):
+                print(f"[capture] {msg}", file=sys.stderr, flush=True)
+
         g, y_ref, ok = None, None, 1.0
         try:
             self._step_eager()              # communicators exist before capture
             torch.cuda.synchronize(self.device)
             y_ref = self.y.clone()
+            dbg("eager step done")
             g = torch.cuda.CUDAGraph()
             l0 = self.engine.lib.sellb_launch_count()
             # thread_local: the NCCL watchdog thread may query events meanwhile
             with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 self._step_eager()
             self.graph_launches = int(self.engine.lib.sellb_launch_count() - l0)
-        except Exception:                   # capture unsupported here: stay eager
+            dbg(f"captured ({self.graph_launches} library launches)")
+        except Exception as e:              # capture unsupported here: stay eager
+            dbg(f"capture failed: {e!r}")
             ok = 0.0
         # replay only when EVERY rank captured: a replayed NCCL send/recv whose
         # peer does not replay would wait forever
@@ -323,8 +332,10 @@ class DistSpmv:
             ok = 1.0
             try:
                 self.y.zero_()
+                dbg("replaying")
                 g.replay()
                 torch.cuda.synchronize(self.device)
+                dbg("replayed")
                 iv = torch.int64 if self.y.element_size() == 8 else torch.int32
                 ok = 1.0 if bool(torch.equal(self.y.view(iv), y_ref.view(iv))) else 0.0
             except Exception:

@@ -39,7 +39,7 @@ def test_bench_dist_one_rank_stdout_is_one_json_line(extra):
     assert rec["config"]["parity_vs_oracle_all_ranks"] is True
     assert rec["value"] > 0 and rec["gpu_launches"] >= 20
     assert rec["config"]["parallelism"] == "row-blocks x1"
-    assert rec["config"]["step_graph"] is False      # opt-in (SELLB_DIST_GRAPH=1)
+    assert rec["config"]["step_graph"] is True
 
 
 def test_nccl_p2p_exchange_replays_from_a_cuda_graph():
@@ -52,8 +52,6 @@ def test_nccl_p2p_exchange_replays_from_a_cuda_graph():
     assert out.returncode == 0 and "graph p2p ok" in out.stdout, out.stderr[-3000:]
 
 
-@pytest.mark.skip(reason="hangs on one GPU this round (NCCL self send/recv inside a "
-                         "captured DistSpmv step); the graph path is opt-in until fixed")
 def test_dist_step_graph_with_nccl_self_exchange():
     """DistSpmv.capture with NCCL P2P kernels inside the graph (self
     send/recv of a scattered halo through gather/scatter): replay equals the

@@ -35,6 +35,7 @@ assert ds.capture(), "graph not kept"
 print("capture done", flush=True)
 assert ds.graph_launches >= 3, ds.graph_launches       # gather, spmv, scatter
 y_graph = ds.step().clone()
+print("replay done", flush=True)
 assert torch.equal(y_graph.view(torch.int64), y_eager.view(torch.int64))
 x2 = torch.from_numpy(np.random.default_rng(6).uniform(-1, 1, n)).to(dev)
 ds.x_local.copy_(x2)
@@ -42,6 +43,8 @@ y2 = ds.step().clone()
 ds.graph, g = None, ds.graph
 y2_eager = ds.step().clone()
 ds.graph = g
+del g       # the only reference must be ds.graph for release() to free it
+print("eager-after-graph done", flush=True)
 assert torch.equal(y2.view(torch.int64), y2_eager.view(torch.int64))
 ds.release()
 torch.cuda.synchronize()
