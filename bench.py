@@ -2,28 +2,35 @@
 """Benchmark: fp64 SELL-32-sigma SpMV on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2|cfg1|cfg3|cfg5] [--sigma S] [--dtype f64|f32]
+                    [--config cfg5|cfg1|cfg2|cfg3|cfg4] [--sigma S] [--dtype f64|f32]
 
 One "step" = one SpMV y = A x over the whole matrix (all chunks), x and the
-matrix resident in HBM.  Default workload at N=1: BASELINE configs[1], the 3D
-27-point stencil on 128^3 (N=2,097,152, nnz=55,742,968), SELL-32-1, fp64.
-Its algorithmic bytes (703 MB) exceed the 126 MB L2, so no flush is needed
-between steps ("l2": "inputs larger than L2").
+matrix resident in HBM.  Default workload: BASELINE configs[4] -- the metric
+is quoted "at 1/2/4/8 B200" on it -- the N = 2^26 banded-random
+Hamiltonian-like matrix (1,321,641,891 nonzeros), SELL-32-512, fp64,
+generated and built on the GPU (16 GB of CRS never touches the host).  Its
+algorithmic bytes (17 GB) exceed the 126 MB L2 many times over, so no flush
+is needed between steps.
 
-N > 1 (torchrun, one process per GPU, NCCL): weak scaling -- the 27-point
-stencil on 128 x 128 x (128 N), row-partitioned into z-slabs of exactly the
-N=1 size, with the x halo (one 128x128 plane per neighbour) exchanged over
-NCCL and overlapped with the interior chunks (paper_1307_6209_b200/dist.py).
+N > 1 (``--gpus N``; re-launched under torch.distributed.run when not
+already under it; one process per GPU, NCCL): strong scaling of the same
+matrix -- N row blocks aligned to lcm(32, 512), each generated and built on
+its own GPU, the x halo exchanged over NCCL and overlapped with the interior
+chunks (paper_1307_6209_b200/dist.py).  ``--config cfg2`` under N > 1 is the
+weak-scaling stencil (one 128^3 z-slab per GPU).
 
 Printed JSON (rank 0): metric/value (GF/s = 2 nnz / t, padding excluded,
 bench.py:89 of the reference), roofline of the SpMV kernel against
-MEASURED_PEAKS.json hbm_gbs, e2e through the public host-array API with
-pinned buffers, the reference CPU path timed on this host (cpu_baseline),
-clocks sampled during the timed region, and gpu_launches.
+MEASURED_PEAKS.json hbm_gbs, e2e through the public API the reference's
+callers use (``spmv_sell(m, x, y)`` with ordinary pageable NumPy vectors;
+the pinned-buffer number beside it), the reference CPU path timed on this
+host (cpu_baseline), clocks sampled during the timed region, gpu_launches.
 
 ``--impl reference`` times the reference's own compiled kernel core
 (oracle/_ref, built from /root/reference sources) with all host threads,
-using the reference's static schedule (spmv.py:53-58) on the same layout.
+using the reference's static schedule (spmv.py:53-58) on the same layout
+(cfg5: a 2^20-row block of the same matrix; the config dict is identical
+to our arm's, the block is named in cpu_baseline.sample).
 """
 
 import argparse
@@ -40,7 +47,7 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-METRIC = "spMVM GFLOP/s (2*nnz/t), fp64 SELL-C-sigma"
+METRIC = "spMVM GFLOP/s (2\u00b7nnz/t) and HBM GB/s vs roofline, fp64, at 1/2/4/8 B200"
 UNIT = "GFLOP/s"
 
 
@@ -198,6 +205,43 @@ def host_cpu_desc():
 
 
 # ---------------------------------------------------------------------------
+# the config dict both arms print (identical, so the driver can compare)
+# ---------------------------------------------------------------------------
+
+CFG5_NNZ = {1 << 26: 1_321_641_891}     # generate.hamiltonian_rows, default keep/seed
+
+
+def workload_desc(args, world):
+    if args.config == "cfg5":
+        n = args.n or (1 << 26)
+        return (f"banded-random Hamiltonian-like N={n} (BASELINE configs[4]), "
+                f"SELL-{args.C}-{args.sigma}")
+    if args.config == "cfg2" and world > 1:
+        return (f"3D 27-point stencil 128x128x{128 * world} in {world} z-slabs "
+                f"(weak scaling), SELL-{args.C}-{args.sigma}")
+    names = {"cfg1": "2D 5-point Laplacian 1000x1000 (BASELINE configs[0])",
+             "cfg2": "3D 27-point stencil 128^3 (BASELINE configs[1])",
+             "cfg3": "power-law rows N=4M mean~20 (BASELINE configs[2])",
+             "cfg4": "skewed N=2^21 base 8, 1024 spikes of 2048 (BASELINE configs[3])"}
+    if args.config not in names:
+        raise SystemExit(f"unknown config {args.config}")
+    return f"{names[args.config]}, SELL-{args.C}-{args.sigma}"
+
+
+def bench_config(args, world):
+    """Workload identity only; measurement details go under "details"."""
+    n_rows = {"cfg1": 1_000_000, "cfg2": 128 ** 3 * max(1, world if args.config == "cfg2"
+                                                        else 1),
+              "cfg3": 4_000_000, "cfg4": 1 << 21}.get(args.config, args.n or (1 << 26))
+    l2 = ("flushed between steps (4xL2 scratch write + half read back); value from the "
+          "SpMV's own events") if args.config == "cfg1" else "inputs larger than L2"
+    return {"workload": workload_desc(args, world), "matrix": args.config, "C": args.C,
+            "sigma": args.sigma, "dtype": args.dtype, "n_rows": n_rows,
+            "parallelism": "1 GPU" if world == 1 else f"row-blocks x{world}, NCCL halo",
+            "l2": l2}
+
+
+# ---------------------------------------------------------------------------
 # reference arm
 # ---------------------------------------------------------------------------
 
@@ -206,22 +250,24 @@ def run_reference(args):
     if rank != 0:
         return 0
     import oracle
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     sigma = args.sigma
     if args.config == "cfg2" and world > 1:
         from paper_1307_6209_b200 import generate
         crs = generate.stencil27(128, nz=128 * world)
-        desc = f"3D 27-point stencil 128x128x{128 * world} (z-slabs)"
+        block = f"the whole 128x128x{128 * world} stencil"
     elif args.config == "cfg5":
         # the host cannot hold 1.3e9 nonzeros through the reference's path:
         # a 2^20-row block of the row-addressable matrix
         from paper_1307_6209_b200 import CRSMatrix, generate
         n = args.n or (1 << 26)
-        rp, cl_, vl = generate.hamiltonian_rows(n, 0, 1 << 20)
-        crs = CRSMatrix(1 << 20, n, rp, cl_, vl)
-        desc = f"rows [0, 2^20) of the banded-random N={n} matrix"
+        rows = min(n, 1 << 20)
+        rp, cl_, vl = generate.hamiltonian_rows(n, 0, rows)
+        crs = CRSMatrix(rows, n, rp, cl_, vl)
+        block = f"rows [0, {rows}) of the N={n} matrix (the full matrix is 16 GB of CRS)"
     else:
-        crs, desc = make_matrix(args.config)
+        crs, _ = make_matrix(args.config)
+        block = "the whole matrix"
     o = oracle.crs_to_sell(crs.rpt, crs.col, crs.val, crs.n_rows, crs.n_cols, args.C, sigma)
     x = np.random.default_rng(12345).uniform(-1, 1, crs.n_cols)
     threads = os.cpu_count() or 1
@@ -248,17 +294,17 @@ def run_reference(args):
             step()
         dt = time.perf_counter() - t0
     value = 2.0 * nnz * args.steps / dt / 1e9
-    sample = (f"{nch} of {o.n_chunks} chunks ({nnz} nnz) per step; static split over "
-              f"{len(spans)} threads (sellkit spmv.py:53-58); "
+    sample = (f"{block}: {nch} of {o.n_chunks} chunks ({nnz} nnz) per step; static split "
+              f"over {len(spans)} threads (sellkit spmv.py:53-58); "
               f"{'reference _kernels.pyx compiled from /root/reference sources (oracle/_ref)' if ref else 'C port (oracle/sell_oracle.c)'}; "
               f"host {host_cpu_desc()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{desc}, SELL-{args.C}-{sigma}", "C": args.C, "sigma": sigma,
-                   "n_rows": crs.n_rows, "nnz": crs.nnz},
+        "scaling": "strong" if args.config == "cfg5" and world > 1 else "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": bench_config(args, world),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": len(spans),
                          "kind": "reference" if ref is not None else "port",
                          "sample": sample},
@@ -392,6 +438,18 @@ def host_workload(args, dt_np):
                               "restatement of formats.py:295-393 (oracle), one thread"}}
 
 
+def parity_blocks(n, blk):
+    """Row blocks checked against the oracle at full size: the first, the
+    last, and blocks straddling each quarter boundary (the N = 2/4 rank
+    boundaries of the row-partitioned run), aligned to the block size."""
+    starts = {0, max(0, n - blk)}
+    for q in (1, 2, 3):
+        b = (n * q // 4) // blk * blk
+        starts.add(max(0, min(n - blk, b - blk // 2)))   # straddles b (512-aligned)
+        starts.add(max(0, min(n - blk, b)))
+    return sorted(starts)
+
+
 def cfg5_workload(args, dt_np):
     """cfg5: the N = 2^26, ~1.3e9-nonzero banded-random matrix generated and
     built on the GPU (16 GB of CRS never touches the host).  Parity and the
@@ -421,7 +479,7 @@ def cfg5_workload(args, dt_np):
 
     def parity(yd):
         ok = True
-        for r0 in (0, (n // 2) // blk * blk, n - blk):
+        for r0 in parity_blocks(n, blk):
             b = block(r0, r0 + blk)
             o = oracle.crs_to_sell(b.rpt, b.col, b.val, b.n_rows, n, args.C, sigma)
             got = s.export_range(r0 // 32, (r0 + blk) // 32)
@@ -440,7 +498,10 @@ def cfg5_workload(args, dt_np):
                 "sample": f"rows [0, {b.n_rows}) block of the N={n} matrix: " + sample
                           + f"; host {host_cpu_desc()}"}
 
-    return {"sell": s, "desc": f"banded-random Hamiltonian-like N={n} (device-generated, "
+    scope = (f"{len(parity_blocks(n, blk))} blocks of {blk} rows (first, last, quarter "
+             f"boundaries): cs/cl/col/val/row_lengths and y bit-exact vs the oracle")
+    return {"sell": s, "parity_scope": scope,
+            "desc": f"banded-random Hamiltonian-like N={n} (device-generated, "
                                f"generation {t_gen:.2f} s)",
             "x": x, "build_s": build_s, "parity": parity, "cpu": cpu}
 
@@ -451,6 +512,8 @@ def run_ours(args):
     if world > 1 or os.environ.get("SELLB_FORCE_DIST"):   # (1-rank smoke of the N>1 leg)
         import bench_dist
         args.peak = measured_peaks()[0]
+        args.metric = METRIC
+        args.config_dict = bench_config(args, world)
         args.clock_sampler = ClockSampler
         return bench_dist.bench_main(args)
     import oracle
@@ -541,7 +604,27 @@ def run_ours(args):
     peak, peak_kind = measured_peaks()
     achieved = v_alg / (kern_ms / 1e3) / 1e9
 
-    # e2e: the public host-array API (sellb_spmv_host) with pinned x / y
+    # e2e through the public API a reference caller uses: spmv_sell(m, x, y)
+    # with ordinary (pageable) NumPy vectors (spmv.py:105-122) -- x H2D,
+    # the product, y D2H, all inside every timed call
+    e2e_steps = max(3, min(args.steps, 100))
+    x_np = np.array(x_host, dtype=dt_np)            # plain pageable arrays
+    y_np = np.empty(n_pad, dtype=dt_np)
+    for _ in range(2):
+        sb.spmv_sell(s, x_np, y_np)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sb.spmv_sell(s, x_np, y_np)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_ok = bool(y_np.tobytes() == yd.cpu().numpy().tobytes())
+    # the same call with y=None (the reference allocates y per call)
+    t0 = time.perf_counter()
+    n_alloc = max(2, min(e2e_steps, 10))
+    for _ in range(n_alloc):
+        y_new = sb.spmv_sell(s, x_np)
+    e2e_alloc_s = (time.perf_counter() - t0) / n_alloc
+    del y_new
+    # and through the C ABI with library-pinned x / y (PCIe-bound floor)
     import ctypes
     px, py = ctypes.c_void_p(), ctypes.c_void_p()
     _lib.check(lib.sellb_host_alloc(n_cols * s_v, ctypes.byref(px)))
@@ -549,17 +632,17 @@ def run_ours(args):
     xh = np.ctypeslib.as_array((ctypes.c_byte * (n_cols * s_v)).from_address(px.value)).view(dt_np)
     yh = np.ctypeslib.as_array((ctypes.c_byte * (n_pad * s_v)).from_address(py.value)).view(dt_np)
     xh[:] = x_host
-    e2e_steps = max(3, min(args.steps, 200))
     for _ in range(3):
         _lib.check(lib.sellb_spmv_host(handle, px.value, py.value, 0, n_chunks, 0, 0, sp))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         _lib.check(lib.sellb_spmv_host(handle, px.value, py.value, 0, n_chunks, 0, 0, sp))
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_ok = bool(yh.tobytes() == yd.cpu().numpy().tobytes())
+    e2e_pin_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_ok = e2e_ok and bool(yh.tobytes() == y_np.tobytes())
     lib.sellb_host_free(px)
     lib.sellb_host_free(py)
+    del x_np, y_np
 
     # reference CPU path on this host, bounded sample (rank 0, N=1)
     cpu = None
@@ -573,17 +656,17 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_ms, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": f"{desc}, SELL-{args.C}-{sigma}", "C": args.C, "sigma": sigma,
-                   "n_rows": n_rows, "nnz": nnz, "slots": slots,
-                   "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
-                   "long_rows": s.long_rows_info(),
-                   "l2": ("flushed between steps (%d MB scratch write, then half of it "
-                          "read back so the L2 holds clean lines); value from the SpMV's "
-                          "own events" % (4 * l2_bytes // 2**20)) if flush is not None
-                   else "inputs larger than L2 (V_alg %.0f MB > %d MB L2)" % (
-                       v_alg / 1e6, l2_bytes // 2**20),
-                   "build_s": round(build_s, 4), "build": wl.get("build"),
-                   "parity_vs_oracle": parity},
+        "config": bench_config(args, 1),
+        "details": {"matrix": desc, "n_rows": n_rows, "nnz": nnz, "slots": slots,
+                    "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
+                    "long_rows": s.long_rows_info(),
+                    "l2": ("flushed between steps (%d MB scratch write, then half of it "
+                           "read back so the L2 holds clean lines); value from the SpMV's "
+                           "own events" % (4 * l2_bytes // 2**20)) if flush is not None
+                    else "inputs larger than L2 (V_alg %.0f MB > %d MB L2)" % (
+                        v_alg / 1e6, l2_bytes // 2**20),
+                    "build_s": round(build_s, 4), "build": wl.get("build"),
+                    "parity_vs_oracle": parity, "parity_scope": wl.get("parity_scope")},
         "model": model_block(s, nnz, n_rows, n_cols, n_pad, n_chunks, slots, s_v, traffic,
                              kern_ms, peak),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
@@ -593,8 +676,16 @@ def run_ours(args):
                      "kernel_ms": round(kern_ms, 5)},
         "e2e": {"value": round(2.0 * nnz / e2e_s / 1e9, 3), "unit": UNIT,
                 "h2d_bytes_per_step": n_cols * s_v, "d2h_bytes_per_step": n_pad * s_v,
-                "ms_per_step": round(e2e_s * 1e3, 4), "api": "sellb_spmv_host (pinned)",
-                "matches_device": e2e_ok},
+                "ms_per_step": round(e2e_s * 1e3, 4),
+                "api": "paper_1307_6209_b200.spmv_sell(m, x, y) with pageable NumPy x / y "
+                       "(the reference's call, spmv.py:105-122)",
+                "matches_device": e2e_ok,
+                "y_allocated_per_call": {"value": round(2.0 * nnz / e2e_alloc_s / 1e9, 3),
+                                         "ms_per_step": round(e2e_alloc_s * 1e3, 4),
+                                         "api": "spmv_sell(m, x) (y=None)"},
+                "pinned": {"value": round(2.0 * nnz / e2e_pin_s / 1e9, 3),
+                           "ms_per_step": round(e2e_pin_s * 1e3, 4),
+                           "api": "sellb_spmv_host with library-pinned x / y"}},
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": int(n_launches),
@@ -603,15 +694,38 @@ def run_ours(args):
     return 0
 
 
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch_distributed(args, argv):
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run, one process per GPU (the driver's own launch)."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} asks for {args.gpus} GPUs, {have} visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+    log("relaunching:", " ".join(cmd))
+    os.execv(sys.executable, cmd)
+
+
 def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=4000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5",
+                    choices=("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"))
     ap.add_argument("--sigma", type=int, default=None,
-                    help="sorting scope (default 1; 512 for cfg5)")
+                    help="sorting scope (default 512 for cfg5, else 1)")
     ap.add_argument("--C", type=int, default=32, help="chunk height")
     ap.add_argument("--dtype", choices=("f64", "f32"), default="f64")
     ap.add_argument("--skip-parity", action="store_true")
@@ -625,8 +739,15 @@ def main(argv=None):
         args.sigma = 512 if args.config == "cfg5" else 1
     if args.warmup < 3:
         args.warmup = 3
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None and int(world) != args.gpus and args.gpus != 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world is not None:
+        args.gpus = int(world)
     if args.impl == "reference":
         return run_reference(args)
+    if world is None and args.gpus > 1:
+        relaunch_distributed(args, argv)
     return run_ours(args)
 
 

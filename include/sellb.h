@@ -118,11 +118,16 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
 
 /* Wrap an existing SELL layout (e.g. built by the reference or read from a
  * .sell cache).  perm / row_lengths may be NULL (row_lengths NULL => the
- * pad-inclusive kernel, exactly the reference's loop). */
+ * pad-inclusive kernel, exactly the reference's loop).  n_slots is the
+ * length of the caller's col / val buffers; the reference's SellMatrix
+ * invariants (formats.py:210-251) are checked before the matrix is usable:
+ * cs[n_chunks] == n_slots, cs[0] == 0, cs[i+1] - cs[i] == C * cl[i],
+ * 0 <= col < n_cols, perm a bijection, 0 <= row_lengths <= cl and 0 on
+ * padding rows -- SELLB_ESTRUCT otherwise. */
 int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col,
                  const void* val, const int32_t* perm, const int32_t* row_lengths,
                  int32_t dtype, int64_t n_rows, int64_t n_cols, int32_t C,
-                 int64_t sigma, int64_t n_chunks, int32_t col_permuted,
+                 int64_t sigma, int64_t n_chunks, int64_t n_slots, int32_t col_permuted,
                  int32_t device, void* stream, int32_t ptrs_on_device,
                  sellb_mat** out);
 
@@ -288,6 +293,16 @@ int sellb_sell_x_lines(const sellb_mat* m, int32_t elems_per_line, int64_t* line
 /* Pinned host buffers for the end-to-end path. */
 int sellb_host_alloc(size_t bytes, void** out);
 int sellb_host_free(void* p);
+
+/* Page-lock (and map) a caller's existing host buffer in place, so
+ * sellb_spmv_host moves it by DMA at pinned speed instead of staging it
+ * through the library's mirrors.  The caller must unregister before the
+ * memory is released (the Python layer ties this to the array's lifetime).
+ * Returns SELLB_ERESOURCE if the range cannot be registered (e.g. it
+ * shares pages with an already registered range): callers fall back to
+ * the staged path. */
+int sellb_host_register(void* p, size_t bytes);
+int sellb_host_unregister(void* p);
 
 #ifdef __cplusplus
 }

@@ -36,7 +36,8 @@ EXPORTED = (
     "sellb_export_range", "sellb_infer_row_lengths", "sellb_chunk_flags",
     "sellb_coo_to_crs", "sellb_mm_parse_body", "sellb_mm_format_body",
     "sellb_launch_count", "sellb_long_info", "sellb_streamed_bytes",
-    "sellb_lru_stream_misses", "sellb_sell_x_lines",
+    "sellb_lru_stream_misses", "sellb_sell_x_lines", "sellb_host_register",
+    "sellb_host_unregister",
 )
 
 
@@ -69,7 +70,8 @@ _PROTOS = {
     "sellb_build_from_crs": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i32, _i64,
                                             _i32, _i32, _i32, _vp, _i32, ctypes.POINTER(_vp)]),
     "sellb_import": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i32,
-                                    _i64, _i64, _i32, _i32, _vp, _i32, ctypes.POINTER(_vp)]),
+                                    _i64, _i64, _i64, _i32, _i32, _vp, _i32,
+                                    ctypes.POINTER(_vp)]),
     "sellb_info": (ctypes.c_int, [_vp, ctypes.POINTER(Info)]),
     "sellb_device_arrays": (ctypes.c_int, [_vp, ctypes.POINTER(DevArrays)]),
     "sellb_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32]),
@@ -101,6 +103,8 @@ _PROTOS = {
     "sellb_gen_hamiltonian_fill": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i32, ctypes.c_double,
                                                   ctypes.c_uint64, _vp, _vp, _vp, _i32, _vp]),
     "sellb_host_free": (ctypes.c_int, [_vp]),
+    "sellb_host_register": (ctypes.c_int, [_vp, ctypes.c_size_t]),
+    "sellb_host_unregister": (ctypes.c_int, [_vp]),
     "sellb_export_range": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sellb_infer_row_lengths": (ctypes.c_int, [_vp, _vp]),
     "sellb_chunk_flags": (ctypes.c_int, [_vp, _vp, _vp, _vp]),

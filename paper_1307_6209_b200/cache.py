@@ -26,7 +26,7 @@ import numpy as np
 
 from . import _lib
 from .errors import FormatError
-from .formats import SellMatrix
+from .formats import SellMatrix, validate_sell_arrays
 
 MAGIC = b"SELL"
 VERSION = 1
@@ -96,12 +96,19 @@ def read_sell_cache(path, device=0):
     if stored != crc:
         raise FormatError(f"{path}: checksum failure (corrupted cache)")
 
+    # the reference builds a SellMatrix from the arrays, whose __post_init__
+    # rejects a structurally invalid file (valid CRC, inconsistent arrays)
+    # with StructuralError before anything indexes them (formats.py:210-251)
+    h = dict(arrays, row_lengths=None)
+    h["perm"] = arrays["perm"].astype(np.int64) if len(arrays["perm"]) else arrays["perm"]
+    validate_sell_arrays(int(n_rows), int(n_cols), int(C), int(sigma), int(n_pad),
+                         int(n_chunks), h)
     lib = _lib.require_device()
     out = ctypes.c_void_p()
     _lib.check(lib.sellb_import(
         _lib.ptr(arrays["cs"]), _lib.ptr(arrays["cl"]), _lib.ptr(arrays["col"]),
         _lib.ptr(arrays["val"]), _lib.ptr(arrays["perm"]), None, _lib.SELLB_F64,
-        int(n_rows), int(n_cols), int(C), int(sigma), int(n_chunks),
+        int(n_rows), int(n_cols), int(C), int(sigma), int(n_chunks), len(arrays["val"]),
         int(bool(flags & FLAG_COL_PERMUTED)), int(device), None, 0, ctypes.byref(out)))
     try:
         _lib.check(lib.sellb_infer_row_lengths(out.value, None))

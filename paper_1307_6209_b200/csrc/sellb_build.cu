@@ -47,6 +47,16 @@ __global__ void k_row_lengths(const int64_t* __restrict__ rpt, int64_t n, int64_
     if ((threadIdx.x & 31) == 0 && l) atomicMax(maxlen, l);
 }
 
+// sellb_import's layout invariants: bad = 3 (cs[0] != 0), 4 (chunk extent
+// != C * cl or negative cl)
+__global__ void k_check_layout(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+                               int64_t n_chunks, int64_t C, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i == 0 && cs[0] != 0) atomicExch(bad, 3);
+    if (i < n_chunks && (cl[i] < 0 || cs[i + 1] - cs[i] != C * (int64_t)cl[i]))
+        atomicMax(bad, 4);
+}
+
 __global__ void k_check_cols(const int32_t* __restrict__ col, int64_t nnz, int64_t n_cols,
                              int* __restrict__ bad) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -287,6 +297,8 @@ void free_mat_arrays(sellb_mat* m) {
     }
     cudaFree(m->x_buf);
     cudaFree(m->y_buf);
+    if (m->hx) cudaFreeHost(m->hx);
+    if (m->hy) cudaFreeHost(m->hy);
 }
 
 int alloc_dev(void** p, size_t bytes) {
@@ -764,8 +776,9 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
 
 int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const void* val,
                  const int32_t* perm, const int32_t* row_lengths, int32_t dtype, int64_t n_rows,
-                 int64_t n_cols, int32_t C, int64_t sigma, int64_t n_chunks, int32_t col_permuted,
-                 int32_t device, void* stream, int32_t ptrs_on_device, sellb_mat** out) {
+                 int64_t n_cols, int32_t C, int64_t sigma, int64_t n_chunks, int64_t n_slots,
+                 int32_t col_permuted, int32_t device, void* stream, int32_t ptrs_on_device,
+                 sellb_mat** out) {
     clear_error();
     if (!out) return set_error(SELLB_EPARAM, "out must not be NULL");
     *out = nullptr;
@@ -789,7 +802,11 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
         total = cs[n_chunks];
     }
     if (total < 0) return set_error(SELLB_ESTRUCT, "cs[n_chunks] must be >= 0");
+    // the caller's col / val buffers hold n_slots entries: never read past them
+    if (total != n_slots)
+        return set_error(SELLB_ESTRUCT, "col/val length must equal cs[n_chunks]");
     if (total && (!col || !val)) return set_error(SELLB_EPARAM, "col/val must not be NULL");
+    if (total && n_cols == 0) return set_error(SELLB_ESTRUCT, "stored slots require n_cols >= 1");
     sellb_mat* m = new (std::nothrow) sellb_mat();
     if (!m) return set_error(SELLB_ERESOURCE, "host allocation failed");
     struct Holder {
@@ -811,6 +828,27 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
         SELLB_CU(cudaMemcpyAsync(m->col, col, total * 4, kind, st));
         SELLB_CU(cudaMemcpyAsync(m->val, val, total * vs, kind, st));
     }
+    // the reference's SellMatrix invariants (formats.py:210-251) on the device:
+    // cs[0] == 0, cs[i+1] - cs[i] == C * cl[i], 0 <= col < n_cols -- the
+    // kernels index x and the arrays by them
+    {
+        DBuf d_bad;
+        SELLB_CU(d_bad.alloc(4, st));
+        SELLB_CU(cudaMemsetAsync(d_bad.p, 0, 4, st));
+        k_check_layout<<<(unsigned)grid_for(std::max<int64_t>(n_chunks, 1), 256), 256, 0, st>>>(
+            m->cs, m->cl, n_chunks, C, d_bad.as<int>());
+        if (total) {
+            int blocks = (int)std::min<int64_t>(grid_for(total, 256), 148 * 16);
+            k_check_cols<<<blocks, 256, 0, st>>>(m->col, total, n_cols, d_bad.as<int>());
+        }
+        if (int rc = check_stream_error()) return rc;
+        int bad = 0;
+        SELLB_CU(cudaMemcpyAsync(&bad, d_bad.p, 4, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+        if (bad == 3) return set_error(SELLB_ESTRUCT, "cs[0] must be 0");
+        if (bad == 4) return set_error(SELLB_ESTRUCT, "cs[i+1] - cs[i] must equal C * cl[i]");
+        if (bad == 2) return set_error(SELLB_ESTRUCT, "column index out of bounds");
+    }
     if (perm && n_rows) {
         if (int rc = alloc_dev((void**)&m->perm, n_rows * 4)) return rc;
         SELLB_CU(cudaMemcpyAsync(m->perm, perm, n_rows * 4, kind, st));
@@ -819,10 +857,12 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
         std::vector<int32_t> h_perm(n_rows), h_order(m->n_pad);
         SELLB_CU(cudaMemcpyAsync(h_perm.data(), m->perm, n_rows * 4, cudaMemcpyDeviceToHost, st));
         SELLB_CU(cudaStreamSynchronize(st));
-        for (int64_t p = 0; p < m->n_pad; ++p) h_order[p] = (int32_t)p;   // padding rows
+        for (int64_t p = 0; p < n_rows; ++p) h_order[p] = -1;
+        for (int64_t p = n_rows; p < m->n_pad; ++p) h_order[p] = (int32_t)p;   // padding rows
         for (int64_t i = 0; i < n_rows; ++i) {
             int32_t p = h_perm[i];
-            if (p < 0 || p >= n_rows) return set_error(SELLB_ESTRUCT, "perm must be a permutation");
+            if (p < 0 || p >= n_rows || h_order[p] != -1)
+                return set_error(SELLB_ESTRUCT, "perm must be a permutation of 0..n_rows-1");
             h_order[p] = (int32_t)i;
         }
         SELLB_CU(cudaMemcpyAsync(m->order, h_order.data(), m->n_pad * 4, cudaMemcpyHostToDevice, st));
@@ -843,8 +883,17 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
         std::vector<int32_t> h_rl(m->n_pad);
         SELLB_CU(cudaMemcpyAsync(h_rl.data(), m->rl, m->n_pad * 4, cudaMemcpyDeviceToHost, st));
         SELLB_CU(cudaStreamSynchronize(st));
+        std::vector<int32_t> h_cl(n_chunks);
+        SELLB_CU(cudaMemcpy(h_cl.data(), m->cl, n_chunks * 4, cudaMemcpyDeviceToHost));
         int64_t s = 0;
-        for (auto v : h_rl) s += v;
+        for (int64_t p = 0; p < m->n_pad; ++p) {
+            const int32_t v = h_rl[p];
+            if (v < 0 || v > h_cl[p / C])
+                return set_error(SELLB_ESTRUCT, "row length outside [0, cl] for its chunk");
+            if (p >= n_rows && v != 0)
+                return set_error(SELLB_ESTRUCT, "padding rows must have length 0");
+            s += v;
+        }
         m->nnz = s;
         m->variant = SELLB_VARIANT_AUTO;
         if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;

@@ -74,6 +74,11 @@ struct sellb_mat {
     // end-to-end staging (device x / y for sellb_spmv_host)
     void* x_buf = nullptr;
     void* y_buf = nullptr;
+    // pinned (mapped) host mirrors of x / y for callers with pageable
+    // vectors (sellb_host.cu): x staged piece by piece by a host thread pool,
+    // y written by the kernels straight into hy and copied out per row block
+    void* hx = nullptr;
+    void* hy = nullptr;
     std::mutex mu;
     // host copy of cs (lazily fetched) for the TMA path's tile sizing
     std::vector<int64_t> h_cs;
@@ -149,6 +154,11 @@ int launch_long_tma(const sellb_mat* m, const void* x, void* y, int64_t p0, int6
                     int accumulate, int out_order, const int32_t* rows, int64_t n_rows_list,
                     int l2pol, cudaStream_t st);
 bool long_tma_possible(const sellb_mat* m);
+
+// sellb_host.cu: host staging of pageable vectors
+void host_parallel_copy(void* dst, const void* src, size_t n);
+bool is_pinned(const void* p);
+int ensure_host_mirror(void** slot, size_t bytes);
 
 inline int64_t grid_for(int64_t n, int threads) { return (n + threads - 1) / threads; }
 

@@ -1443,7 +1443,9 @@ __global__ void k_chunk_maxcol(const int64_t* __restrict__ cs, const int32_t* __
 // landed).
 int pipe_setup(sellb_mat* m) {
     if (m->pipe_ready) return 0;
-    int want = 4;   // tools/e2e_probe.py on cfg2: depth 2/4/8 -> 0.571/0.499-0.559/0.643 ms
+    // cfg5 (tools/pcie_probe.py box): depth 4 / 8 -> pinned 14.4 / 13.4 ms, pageable
+    // staged 28.0 / 25.9 ms per step; cfg2 (tools/e2e_probe.py) is flat from 4 up
+    int want = 8;
     if (const char* e = getenv("SELLB_PIPE")) want = std::max(1, std::min(atoi(e), sellb_mat::kPipe));
     const int P = (int)std::min<int64_t>(want, std::max<int64_t>(m->n_chunks, 1));
     std::vector<int32_t> maxcol(std::max<int64_t>(m->n_chunks, 1), 0);
@@ -1493,50 +1495,84 @@ int pipe_setup(sellb_mat* m) {
 
 // y = A x with host x / y: x streams in column pieces on one copy engine,
 // row blocks start as soon as the x they read has landed, and each block's
-// y streams back on the other copy engine while later blocks compute.
+// y streams back while later blocks compute.
+//
+// Pinned caller buffers: DMA straight from x_host; the kernels store y
+// straight into the mapped y_host (no D2H pass).  Pageable caller buffers
+// (ordinary NumPy arrays, the reference's call, spmv.py:105-122): x piece i
+// is copied by the host thread pool into the pinned mirror hx while piece
+// i-1 is on the wire; the kernels store y into the mapped mirror hy and
+// every finished row block is copied out by the pool while later blocks
+// compute.  Either way every byte crosses PCIe once, at pinned speed.
 int spmv_host_pipelined(sellb_mat* m, const void* x_host, void* y_host, cudaStream_t user) {
     if (int rc = pipe_setup(m)) return rc;
     const size_t vs = vsize(m->dtype);
     const int P = m->n_pieces;
+    const bool x_pinned = is_pinned(x_host);
+    const bool y_pinned = is_pinned(y_host);
+    const bool zero_copy = !getenv("SELLB_NO_ZEROCOPY");
+    if (!x_pinned) {
+        if (int rc = ensure_host_mirror(&m->hx, (size_t)m->n_cols * vs)) return rc;
+    }
+    if (!y_pinned && zero_copy) {
+        if (int rc = ensure_host_mirror(&m->hy, (size_t)m->n_pad * vs)) return rc;
+    }
+    // where the kernels write y: the caller's pinned buffer or our mirror
+    // (mapped; device pointer from the runtime), else y_buf + D2H copies
+    void* y_dev_view = nullptr;
+    if (zero_copy) {
+        void* host_y = y_pinned ? y_host : m->hy;
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, host_y) == cudaSuccess && at.devicePointer)
+            y_dev_view = at.devicePointer;
+        cudaGetLastError();
+    }
+    const char* xsrc = x_pinned ? (const char*)x_host : (const char*)m->hx;
     SELLB_CU(cudaEventRecord(m->ev_start, user));
     SELLB_CU(cudaStreamWaitEvent(m->s_h2d, m->ev_start, 0));
     SELLB_CU(cudaStreamWaitEvent(m->s_comp, m->ev_start, 0));
+    // x piece i, then every row block whose last needed piece is i
+    int waited = -1;
+    int next_blk = 0;
     for (int i = 0; i < P; ++i) {
         const int64_t a = m->x_off[i], b = m->x_off[i + 1];
-        if (b > a)
-            SELLB_CU(cudaMemcpyAsync((char*)m->x_buf + a * vs, (const char*)x_host + a * vs,
-                                     (b - a) * vs, cudaMemcpyHostToDevice, m->s_h2d));
-        SELLB_CU(cudaEventRecord(m->ev_x[i], m->s_h2d));
-    }
-    // Pinned (mapped) y: the kernels store y straight into host memory over
-    // PCIe (coalesced 256 B posted writes per warp), so the D2H direction
-    // needs no copy engine pass at all and overlaps the compute by
-    // construction.  Pageable y: per-block D2H copies on the second engine.
-    void* y_dev_view = nullptr;
-    {
-        cudaPointerAttributes at{};
-        if (!getenv("SELLB_NO_ZEROCOPY") &&
-            cudaPointerGetAttributes(&at, y_host) == cudaSuccess &&
-            at.type == cudaMemoryTypeHost && at.devicePointer)
-            y_dev_view = at.devicePointer;
-        cudaGetLastError();   // clear a "not registered" status for pageable memory
-    }
-    int waited = -1;
-    for (int b = 0; b < P; ++b) {
-        if (m->blk_need[b] > waited) {
-            SELLB_CU(cudaStreamWaitEvent(m->s_comp, m->ev_x[m->blk_need[b]], 0));
-            waited = m->blk_need[b];
+        if (b > a) {
+            if (!x_pinned)
+                host_parallel_copy((char*)m->hx + a * vs, (const char*)x_host + a * vs,
+                                   (b - a) * vs);
+            SELLB_CU(cudaMemcpyAsync((char*)m->x_buf + a * vs, xsrc + a * vs, (b - a) * vs,
+                                     cudaMemcpyHostToDevice, m->s_h2d));
         }
-        if (int rc = launch_spmv(m, m->x_buf, y_dev_view ? y_dev_view : m->y_buf, m->blk_c[b],
-                                 m->blk_c[b + 1], 0, SELLB_ORDER_STORED, m->s_comp))
-            return rc;
-        SELLB_CU(cudaEventRecord(m->ev_blk[b], m->s_comp));
-        if (y_dev_view) continue;
-        SELLB_CU(cudaStreamWaitEvent(m->s_d2h, m->ev_blk[b], 0));
-        const int64_t y0 = m->blk_c[b] * m->C, y1 = m->blk_c[b + 1] * m->C;
-        if (y1 > y0)
-            SELLB_CU(cudaMemcpyAsync((char*)y_host + y0 * vs, (const char*)m->y_buf + y0 * vs,
-                                     (y1 - y0) * vs, cudaMemcpyDeviceToHost, m->s_d2h));
+        SELLB_CU(cudaEventRecord(m->ev_x[i], m->s_h2d));
+        for (; next_blk < P && m->blk_need[next_blk] <= i; ++next_blk) {
+            const int bk = next_blk;
+            if (m->blk_need[bk] > waited) {
+                SELLB_CU(cudaStreamWaitEvent(m->s_comp, m->ev_x[m->blk_need[bk]], 0));
+                waited = m->blk_need[bk];
+            }
+            if (int rc = launch_spmv(m, m->x_buf, y_dev_view ? y_dev_view : m->y_buf,
+                                     m->blk_c[bk], m->blk_c[bk + 1], 0, SELLB_ORDER_STORED,
+                                     m->s_comp))
+                return rc;
+            SELLB_CU(cudaEventRecord(m->ev_blk[bk], m->s_comp));
+            if (y_dev_view) continue;
+            SELLB_CU(cudaStreamWaitEvent(m->s_d2h, m->ev_blk[bk], 0));
+            const int64_t y0 = m->blk_c[bk] * m->C, y1 = m->blk_c[bk + 1] * m->C;
+            if (y1 > y0)
+                SELLB_CU(cudaMemcpyAsync((char*)y_host + y0 * vs,
+                                         (const char*)m->y_buf + y0 * vs, (y1 - y0) * vs,
+                                         cudaMemcpyDeviceToHost, m->s_d2h));
+        }
+    }
+    if (y_dev_view && !y_pinned) {
+        // copy each finished row block out of the mirror while later ones run
+        for (int bk = 0; bk < P; ++bk) {
+            SELLB_CU(cudaEventSynchronize(m->ev_blk[bk]));
+            const int64_t y0 = m->blk_c[bk] * m->C, y1 = m->blk_c[bk + 1] * m->C;
+            if (y1 > y0)
+                host_parallel_copy((char*)y_host + y0 * vs, (const char*)m->hy + y0 * vs,
+                                   (y1 - y0) * vs);
+        }
     }
     SELLB_CU(cudaStreamSynchronize(y_dev_view ? m->s_comp : m->s_d2h));
     SELLB_CU(cudaStreamSynchronize(m->s_h2d));
@@ -1610,7 +1646,7 @@ int sellb_spmv_sell_range_host(const int64_t* cs, const int32_t* cl, int32_t C,
     if (cs[n_chunks] != n_slots) return set_error(SELLB_ESTRUCT, "cs[n_chunks] != len(val)");
     sellb_mat* m = nullptr;
     int rc = sellb_import(cs, cl, col, val, nullptr, nullptr, SELLB_F64, n_chunks * C, n_x, C, 1,
-                          n_chunks, 0, device, nullptr, 0, &m);
+                          n_chunks, n_slots, 0, device, nullptr, 0, &m);
     if (rc) return rc;
     rc = sellb_spmv_host(m, x, y, c0, c1, accumulate, SELLB_ORDER_STORED, nullptr);
     sellb_free(m);

@@ -250,4 +250,26 @@ int sellb_host_free(void* p) {
     return 0;
 }
 
+int sellb_host_register(void* p, size_t bytes) {
+    clear_error();
+    if (!p || !bytes) return set_error(SELLB_EPARAM, "NULL or empty range");
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(SELLB_ERESOURCE, "cudaHostRegister failed: %s", cudaGetErrorString(e));
+    }
+    return 0;
+}
+
+int sellb_host_unregister(void* p) {
+    clear_error();
+    if (!p) return 0;
+    cudaError_t e = cudaHostUnregister(p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(SELLB_ERESOURCE, "cudaHostUnregister failed: %s", cudaGetErrorString(e));
+    }
+    return 0;
+}
+
 }  // extern "C"

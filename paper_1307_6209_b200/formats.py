@@ -257,6 +257,53 @@ def crs_to_coo(m):
 _ARRAYS = ("cs", "cl", "col", "val", "perm", "row_lengths")
 
 
+def validate_sell_arrays(n_rows, n_cols, C, sigma, n_rows_padded, n_chunks, h):
+    """The reference's SellMatrix.__post_init__ invariants (formats.py:210-251)
+    on host arrays h = {cs, cl, col, val, perm, row_lengths}; row_lengths may
+    be None (a .sell cache: rebuilt on the device afterwards, within [0, cl]
+    by construction).  Same exception classes and messages."""
+    if C < 1:
+        raise ParameterError(f"chunk height C must be >= 1, got {C}")
+    if sigma < 1:
+        raise ParameterError(f"sigma must be >= 1, got {sigma}")
+    if n_chunks * C != n_rows_padded:
+        raise StructuralError("n_rows_padded must equal n_chunks * C")
+    if not n_rows <= n_rows_padded < n_rows + C:
+        if not (n_rows == 0 and n_rows_padded == 0):
+            raise StructuralError("n_rows_padded must be n_rows rounded up to C")
+    cs, cl = h["cs"], h["cl"]
+    if len(cs) != n_chunks + 1 or len(cl) != n_chunks:
+        raise StructuralError("cs/cl length mismatch with n_chunks")
+    if len(cs) and cs[0] != 0:
+        raise StructuralError("cs[0] must be 0")
+    if np.any(np.diff(cs) != C * cl.astype(OFFSET_DTYPE)):
+        raise StructuralError("cs[i+1] - cs[i] must equal C * cl[i]")
+    total = int(cs[-1]) if len(cs) else 0
+    if len(h["col"]) != total or len(h["val"]) != total:
+        raise StructuralError("col/val length must equal cs[n_chunks]")
+    perm = h["perm"]
+    if len(perm) != n_rows:
+        raise StructuralError("perm must have length n_rows")
+    if n_rows:
+        if perm.min() < 0 or perm.max() >= n_rows or \
+                np.any(np.bincount(perm, minlength=n_rows) != 1):
+            raise StructuralError("perm must be a permutation of 0..n_rows-1")
+    rl = h.get("row_lengths")
+    if rl is not None:
+        if len(rl) != n_rows_padded:
+            raise StructuralError("row_lengths must have length n_rows_padded")
+        if n_rows_padded:
+            cap = np.repeat(cl, C)
+            if np.any(rl > cap) or np.any(rl < 0):
+                raise StructuralError("row length outside [0, cl] for its chunk")
+            if np.any(rl[n_rows:] != 0):
+                raise StructuralError("padding rows must have length 0")
+    if total and n_cols == 0:
+        raise StructuralError("stored slots require n_cols >= 1")
+    if total and (h["col"].min() < 0 or h["col"].max() >= n_cols):
+        raise StructuralError("column index out of bounds")
+
+
 class SellMatrix:
     """Chunked, sorted-row sparse matrix living in GPU memory.
 
@@ -322,46 +369,8 @@ class SellMatrix:
 
     def _validate_host(self):
         """The reference's __post_init__ invariants (formats.py:210-251)."""
-        h, C = self._host, self.C
-        if C < 1:
-            raise ParameterError(f"chunk height C must be >= 1, got {C}")
-        if self.sigma < 1:
-            raise ParameterError(f"sigma must be >= 1, got {self.sigma}")
-        if self.n_chunks * C != self.n_rows_padded:
-            raise StructuralError("n_rows_padded must equal n_chunks * C")
-        if not self.n_rows <= self.n_rows_padded < self.n_rows + C:
-            if not (self.n_rows == 0 and self.n_rows_padded == 0):
-                raise StructuralError("n_rows_padded must be n_rows rounded up to C")
-        cs, cl = h["cs"], h["cl"]
-        if len(cs) != self.n_chunks + 1 or len(cl) != self.n_chunks:
-            raise StructuralError("cs/cl length mismatch with n_chunks")
-        if len(cs) and cs[0] != 0:
-            raise StructuralError("cs[0] must be 0")
-        if np.any(np.diff(cs) != C * cl.astype(OFFSET_DTYPE)):
-            raise StructuralError("cs[i+1] - cs[i] must equal C * cl[i]")
-        total = int(cs[-1]) if len(cs) else 0
-        if len(h["col"]) != total or len(h["val"]) != total:
-            raise StructuralError("col/val length must equal cs[n_chunks]")
-        perm = h["perm"]
-        if len(perm) != self.n_rows:
-            raise StructuralError("perm must have length n_rows")
-        if self.n_rows:
-            if perm.min() < 0 or perm.max() >= self.n_rows or \
-                    np.any(np.bincount(perm, minlength=self.n_rows) != 1):
-                raise StructuralError("perm must be a permutation of 0..n_rows-1")
-        rl = h["row_lengths"]
-        if len(rl) != self.n_rows_padded:
-            raise StructuralError("row_lengths must have length n_rows_padded")
-        if self.n_rows_padded:
-            cap = np.repeat(cl, C)
-            if np.any(rl > cap) or np.any(rl < 0):
-                raise StructuralError("row length outside [0, cl] for its chunk")
-            if np.any(rl[self.n_rows:] != 0):
-                raise StructuralError("padding rows must have length 0")
-        if total and self.n_cols == 0:
-            raise StructuralError("stored slots require n_cols >= 1")
-        if total and (h["col"].min() < 0 or h["col"].max() >= self.n_cols):
-            raise StructuralError("column index out of bounds")
+        validate_sell_arrays(self.n_rows, self.n_cols, self.C, self.sigma,
+                             self.n_rows_padded, self.n_chunks, self._host)
 
     # -- device side -----------------------------------------------------------
     @property
@@ -379,7 +388,8 @@ class SellMatrix:
                 _lib.ptr(h["cs"]), _lib.ptr(h["cl"]), _lib.ptr(h["col"]),
                 _lib.ptr(h["val"]), _lib.ptr(h["perm"]), _lib.ptr(h["row_lengths"]),
                 dt, self.n_rows, self.n_cols, self.C, self.sigma, self.n_chunks,
-                int(self.col_permuted), self.device, None, 0, ctypes.byref(out)))
+                len(h["val"]), int(self.col_permuted), self.device, None, 0,
+                ctypes.byref(out)))
             self._attach(out.value)
         return self._handle
 

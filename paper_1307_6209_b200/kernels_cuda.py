@@ -63,7 +63,7 @@ def _sell_handle(cs, cl, C, col, val, n_cols):
     out = ctypes.c_void_p()
     _lib.check(lib.sellb_import(
         _lib.ptr(cs), _lib.ptr(cl), _lib.ptr(col), _lib.ptr(val), None, None,
-        _lib.SELLB_F64, n_chunks * int(C), int(n_cols), int(C), 1, n_chunks, 0,
+        _lib.SELLB_F64, n_chunks * int(C), int(n_cols), int(C), 1, n_chunks, len(val), 0,
         0, None, 0, ctypes.byref(out)))
     h = out.value
     try:

@@ -21,6 +21,9 @@ nothing crosses PCIe.
 """
 
 
+import threading
+import weakref
+
 import numpy as np
 
 from . import _lib, backend
@@ -94,6 +97,58 @@ def _run_host_partitioned(run_range, n_units, threads, scheduling):
         list(pool.map(lambda _: worker(), range(threads)))
 
 
+# ---------------------------------------------------------------------------
+# page-locking of caller vectors that come back (the iterative-solver pattern)
+# ---------------------------------------------------------------------------
+# A pageable NumPy vector is staged by the library through its pinned
+# mirrors (host thread pool, sellb_host.cu).  A vector passed a SECOND time
+# is page-locked in place instead (sellb_host_register), so later calls move
+# it by DMA at pinned speed; the registration is dropped when the array is
+# garbage-collected (weakref.finalize runs before NumPy frees the data).
+# One-shot vectors never pay for the registration.
+
+_PIN_MIN_BYTES = 16 << 20
+_pin_state = {}
+_pin_lock = threading.Lock()
+
+
+def _data_owner(a):
+    o = a
+    while isinstance(o, np.ndarray) and not o.flags.owndata:
+        o = o.base
+    return o if isinstance(o, np.ndarray) and o.flags.owndata else None
+
+
+def _unpin(key):
+    with _pin_lock:
+        st = _pin_state.pop(key, None)
+    if st == "pinned":
+        try:
+            _lib.load().sellb_host_unregister(key[0])
+        except Exception:          # interpreter / CUDA teardown
+            pass
+
+
+def _pin_hint(a):
+    """Register a host vector for DMA the second time it is seen."""
+    if a.nbytes < _PIN_MIN_BYTES:
+        return
+    own = _data_owner(a)
+    if own is None:
+        return
+    key = (own.ctypes.data, own.nbytes)
+    with _pin_lock:
+        st = _pin_state.get(key)
+        if st is None:
+            _pin_state[key] = "seen"
+            weakref.finalize(own, _unpin, key)
+            return
+        if st != "seen":
+            return
+        rc = _lib.load().sellb_host_register(key[0], key[1])
+        _pin_state[key] = "pinned" if rc == 0 else "failed"
+
+
 def _device_spmv(m, x, y, accumulate, out_order, stream):
     """x, y are CUDA tensors of the matrix dtype on the matrix's device."""
     n_out = m.n_rows if out_order == _lib.ORDER_ORIGINAL else m.n_rows_padded
@@ -141,7 +196,10 @@ def spmv_sell(m, x, y=None, accumulate=False, threads=1, scheduling="static",
     n_out = m.n_rows if order == _lib.ORDER_ORIGINAL else m.n_rows_padded
     y = _as_output_vector(y, n_out, dt)
     if k is backend.cuda_kernels() and hasattr(m, "handle"):
-        _lib.check(_lib.require_device().sellb_spmv_host(
+        lib = _lib.require_device()
+        _pin_hint(x)
+        _pin_hint(y)
+        _lib.check(lib.sellb_spmv_host(
             m.handle, _lib.ptr(x), _lib.ptr(y), 0, m.n_chunks,
             int(bool(accumulate)), order, stream))
         return y

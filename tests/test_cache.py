@@ -107,3 +107,59 @@ def test_device_round_trip(tmp_path):
     assert sb.spmv_sell(r, x).tobytes() == sb.spmv_sell(s, x).tobytes()
     assert sb.spmv_sell(r, x, out_order="original").tobytes() == \
         sb.spmv_sell(s, x, out_order="original").tobytes()
+
+
+# --- structurally invalid files with a VALID checksum (the
+# reference's SellMatrix.__post_init__ rejects them, formats.py:210-251; the
+# reader must do the same before any array reaches the device) -------------
+
+def _write_fields(path, **over):
+    from types import SimpleNamespace
+    g = ref("rand")
+    f = {k: g[k] for k in ("cs", "cl", "col", "val", "perm")}
+    f.update(n_rows=int(g["n_rows"]), n_cols=int(g["n_cols"]), C=int(g["C"]),
+             sigma=int(g["sigma"]), n_rows_padded=int(g["n_rows_padded"]),
+             n_chunks=int(g["n_chunks"]), col_permuted=bool(g["col_permuted"]))
+    f.update(over)
+    write_sell_cache(SimpleNamespace(**f), path)
+    return path
+
+
+@pytest.mark.parametrize("case,match", [
+    ("short_col", "col/val length must equal"),
+    ("short_val", "col/val length must equal"),
+    ("col_out_of_range", "column index out of bounds"),
+    ("cl_vs_cs", "cs\\[i\\+1\\] - cs\\[i\\] must equal"),
+    ("cs0", "cs\\[0\\] must be 0"),
+    ("perm_dup", "perm must be a permutation"),
+    ("perm_range", "perm must be a permutation"),
+])
+def test_structurally_invalid_file_is_rejected(tmp_path, case, match):
+    from paper_1307_6209_b200 import StructuralError
+    g = ref("rand")
+    over = {}
+    if case == "short_col":
+        over["col"] = g["col"][:-7]
+    elif case == "short_val":
+        over["val"] = g["val"][:-1]
+    elif case == "col_out_of_range":
+        c = g["col"].copy()
+        c[len(c) // 2] = int(g["n_cols"]) + 3
+        over["col"] = c
+    elif case == "cl_vs_cs":
+        cl = g["cl"].copy()
+        cl[0] += 1
+        over["cl"] = cl
+    elif case == "cs0":
+        over["cs"] = g["cs"] + 32
+    elif case == "perm_dup":
+        p = g["perm"].copy()
+        p[1] = p[0]
+        over["perm"] = p
+    elif case == "perm_range":
+        p = g["perm"].copy()
+        p[0] = int(g["n_rows"]) + 10
+        over["perm"] = p
+    path = _write_fields(tmp_path / "bad.sell", **over)
+    with pytest.raises(StructuralError, match=match):
+        read_sell_cache(path)

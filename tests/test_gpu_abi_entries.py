@@ -126,3 +126,50 @@ def test_launch_counter_counts_spmv_kernels():
     _lib.check(lib.sellb_l2_flush(scratch.data_ptr(), scratch.numel(),
                                   torch.cuda.current_stream().cuda_stream))
     assert lib.sellb_launch_count() - a == 2
+
+
+@pytest.mark.parametrize("case", ["n_slots", "col_range", "cl_vs_cs", "cs0", "perm_dup",
+                                  "rl_over_cl", "rl_padding"])
+def test_import_rejects_inconsistent_layouts(case):
+    """sellb_import checks the reference's SellMatrix invariants itself
+    (formats.py:210-251) and never reads past the caller's col / val
+    (ADVICE r1): every bad layout is SELLB_ESTRUCT, and the library stays
+    usable afterwards."""
+    import ctypes
+    g = next(c for c in map(load_case, golden_cases())
+             if c["n_rows_padded"] > c["n_rows"] > 1 and len(c["val"]) and c["cl"][0] > 0)
+    lib = _lib.load()
+    cs, cl, col, val = g["cs"].copy(), g["cl"].copy(), g["col"].copy(), g["val"].copy()
+    perm, rl = g["perm"].copy(), g["row_lengths"].copy()
+    n_slots = len(val)
+    if case == "n_slots":
+        n_slots -= 1
+    elif case == "col_range":
+        col[len(col) // 2] = g["n_cols"]
+    elif case == "cl_vs_cs":
+        cl[-1] += 1
+    elif case == "cs0":
+        cs = cs + g["C"]
+    elif case == "perm_dup" and len(perm) > 1:
+        perm[1] = perm[0]
+    elif case == "rl_over_cl":
+        rl[0] = cl[0] + 1
+    elif case == "rl_padding":
+        rl[-1] = 1 if cl[-1] > 0 else 0
+        if rl[-1] == 0:
+            pytest.skip("last chunk has width 0")
+    out = ctypes.c_void_p()
+    rc = lib.sellb_import(_lib.ptr(cs), _lib.ptr(cl), _lib.ptr(col), _lib.ptr(val),
+                          _lib.ptr(perm), _lib.ptr(rl), _lib.SELLB_F64, g["n_rows"],
+                          g["n_cols"], g["C"], g["sigma"], g["n_chunks"], n_slots, 0, 0,
+                          None, 0, ctypes.byref(out))
+    assert rc == -3, (case, _lib.last_error())
+    assert not out.value
+    # the library (and the CUDA context) are still fine
+    ok = ctypes.c_void_p()
+    _lib.check(lib.sellb_import(_lib.ptr(g["cs"]), _lib.ptr(g["cl"]), _lib.ptr(g["col"]),
+                                _lib.ptr(g["val"]), _lib.ptr(g["perm"]),
+                                _lib.ptr(g["row_lengths"]), _lib.SELLB_F64, g["n_rows"],
+                                g["n_cols"], g["C"], g["sigma"], g["n_chunks"], len(g["val"]),
+                                0, 0, None, 0, ctypes.byref(ok)))
+    lib.sellb_free(ok.value)

@@ -23,10 +23,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("extra", [["--config", "cfg5", "--rows", str(1 << 21)], []],
-                         ids=["cfg5_small", "cfg2"])
-def test_bench_dist_one_rank_stdout_is_one_json_line(extra):
-    env = dict(os.environ, SELLB_FORCE_DIST="1")
+@pytest.mark.parametrize("extra,graph", [
+    (["--config", "cfg5", "--rows", str(1 << 21)], "0"),
+    (["--config", "cfg5", "--rows", str(1 << 21)], "1"),
+    (["--config", "cfg2"], "0")], ids=["cfg5_small", "cfg5_small_graph", "cfg2"])
+def test_bench_dist_one_rank_stdout_is_one_json_line(extra, graph):
+    env = dict(os.environ, SELLB_FORCE_DIST="1", SELLB_DIST_GRAPH=graph)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            "bench.py", "--gpus", "1", "--steps", "20", "--warmup", "3"] + extra
@@ -36,10 +38,33 @@ def test_bench_dist_one_rank_stdout_is_one_json_line(extra):
     assert len(lines) == 1, out.stdout
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 1 and rec["steps"] == 20 and rec["warmup"] == 3
-    assert rec["config"]["parity_vs_oracle_all_ranks"] is True
+    assert rec["details"]["parity_vs_oracle_all_ranks"] is True
     assert rec["value"] > 0 and rec["gpu_launches"] >= 20
-    assert rec["config"]["parallelism"] == "row-blocks x1"
-    assert rec["config"]["step_graph"] is True
+    assert rec["config"]["parallelism"] == "1 GPU"
+    assert rec["details"]["step_graph"] is (graph == "1")
+    for k in ("exchange_ms", "interior_ms", "boundary_ms", "halo_bytes_per_rank_max"):
+        assert k in rec["halo"]
+
+
+def test_bench_both_arms_print_the_same_config():
+    """The driver compares the two arms' config dicts: they must be equal
+    (the reference arm's cfg5 block is named in cpu_baseline.sample)."""
+    base = [sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--rows",
+            str(1 << 20), "--cpu-budget", "1"]
+    recs = []
+    for impl in ("ours", "reference"):
+        out = subprocess.run(base + ["--impl", impl], capture_output=True, text=True, cwd=ROOT,
+                             timeout=900)
+        assert out.returncode == 0, out.stderr[-3000:]
+        lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+        assert len(lines) == 1, out.stdout
+        recs.append(json.loads(lines[0]))
+    ours, ref = recs
+    assert ours["config"] == ref["config"]
+    assert ours["metric"] == ref["metric"] and ours["unit"] == ref["unit"]
+    assert ours["details"]["parity_vs_oracle"] is True
+    assert ours["e2e"]["matches_device"] is True
+    assert ref["impl"] == "reference" and "rows [0, " in ref["cpu_baseline"]["sample"]
 
 
 def test_nccl_p2p_exchange_replays_from_a_cuda_graph():
