@@ -659,6 +659,7 @@ def run_ours(args):
         "config": bench_config(args, 1),
         "details": {"matrix": desc, "n_rows": n_rows, "nnz": nnz, "slots": slots,
                     "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
+                    "packed_copy": s.packed,
                     "long_rows": s.long_rows_info(),
                     "l2": ("flushed between steps (%d MB scratch write, then half of it "
                            "read back so the L2 holds clean lines); value from the SpMV's "

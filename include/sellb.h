@@ -72,6 +72,7 @@ typedef struct sellb_info_t {
     int32_t variant;        /* resolved SELLB_VARIANT_PAD_SKIP / _PAD_INCL */
     int32_t has_row_lengths;
     int32_t max_cl;
+    int32_t packed;         /* the SpMV streams the packed chunk copy (C = 32, pad-heavy) */
 } sellb_info_t;
 
 /* How the matrix's long rows are handled (rows the bulk role skips):
@@ -153,6 +154,14 @@ int sellb_export_range(const sellb_mat* m, int64_t c0, int64_t c1, int64_t* cs, 
 int sellb_infer_row_lengths(sellb_mat* m, void* stream);
 
 int sellb_set_variant(sellb_mat* m, int32_t variant);
+
+/* Chunk-sorted packed copy for pad-heavy C = 32 layouts: 1 builds it (the
+ * SpMV then streams every short row's entries without padding, bit-identical
+ * sums), 0 drops it, -1 applies the cost model (packed when the pad-skipping
+ * kernel's touched 64-byte sectors exceed the packed bytes by more than
+ * SELLB_PACKED_MIN_GAIN, default 1.15).  Builds leave it off unless the
+ * environment sets SELLB_PACKED=1 or SELLB_PACKED=auto. */
+int sellb_set_packed(sellb_mat* m, int32_t mode);
 void sellb_free(sellb_mat* m);
 
 /* ---- SpMV ---------------------------------------------------------------- */

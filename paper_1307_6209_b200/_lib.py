@@ -37,7 +37,7 @@ EXPORTED = (
     "sellb_coo_to_crs", "sellb_mm_parse_body", "sellb_mm_format_body",
     "sellb_launch_count", "sellb_long_info", "sellb_streamed_bytes",
     "sellb_lru_stream_misses", "sellb_sell_x_lines", "sellb_host_register",
-    "sellb_host_unregister",
+    "sellb_host_unregister", "sellb_set_packed",
 )
 
 
@@ -50,7 +50,7 @@ class Info(ctypes.Structure):
         ("nnz", ctypes.c_int64), ("dtype", ctypes.c_int32),
         ("device", ctypes.c_int32), ("col_permuted", ctypes.c_int32),
         ("variant", ctypes.c_int32), ("has_row_lengths", ctypes.c_int32),
-        ("max_cl", ctypes.c_int32),
+        ("max_cl", ctypes.c_int32), ("packed", ctypes.c_int32),
     ]
 
 
@@ -76,6 +76,7 @@ _PROTOS = {
     "sellb_device_arrays": (ctypes.c_int, [_vp, ctypes.POINTER(DevArrays)]),
     "sellb_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32]),
     "sellb_set_variant": (ctypes.c_int, [_vp, _i32]),
+    "sellb_set_packed": (ctypes.c_int, [_vp, _i32]),
     "sellb_free": (None, [_vp]),
     "sellb_spmv": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp]),
     "sellb_spmv_chunk_list": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _i32, _vp]),

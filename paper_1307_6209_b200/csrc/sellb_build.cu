@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <functional>
@@ -280,6 +281,11 @@ void free_mat_arrays(sellb_mat* m) {
     cudaFree(m->side_off);
     cudaFree(m->side_col);
     cudaFree(m->side_val);
+    cudaFree(m->poff);
+    cudaFree(m->pcol);
+    cudaFree(m->pval);
+    cudaFree(m->prl);
+    cudaFree(m->pidx);
     if (m->pipe_ready) {
         cudaStreamDestroy(m->s_h2d);
         cudaStreamDestroy(m->s_comp);
@@ -548,7 +554,173 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Chunk-sorted packed copy (C = 32; the pJDS idea inside each chunk): the
+// chunk's short rows ordered by descending length (ties by row), stored
+// slot-major without padding -- slot j holds the k_j rows longer than j
+// contiguously, then slot j+1 -- so the SpMV streams each chunk as one dense
+// run of (s_v + 4) bytes per nonzero (k_spmv_packed).  Each row keeps its own
+// slot order, so every sum is unchanged.  Rows the long-row rule hands to the
+// warp-per-row role (chunk wider than long_th and row longer than chunk_th)
+// get length 0 here and sort last.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int packed_len(const int32_t* rl, const int32_t* cl,
+                                          const int32_t* chunk_th, int long_th, int64_t c,
+                                          int lane, bool* is_long) {
+    const int len = rl[c * 32 + lane];
+    *is_long = chunk_th && cl[c] > long_th && len > chunk_th[c];
+    return *is_long ? 0 : len;
+}
+
+__global__ void k_packed_count(const int32_t* __restrict__ rl, const int32_t* __restrict__ cl,
+                               const int32_t* __restrict__ chunk_th, int long_th,
+                               int64_t n_chunks, int64_t* __restrict__ cnt) {
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= n_chunks) return;
+    bool lg;
+    const int len = packed_len(rl, cl, chunk_th, long_th, c, lane, &lg);
+    const int tot = __reduce_add_sync(0xffffffffu, (unsigned)len);
+    if (lane == 0) cnt[c] = tot;
+}
+
+template <typename T>
+__global__ void k_packed_fill(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+                              const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+                              const T* __restrict__ val, const int32_t* __restrict__ chunk_th,
+                              int long_th, int64_t n_chunks, const int64_t* __restrict__ poff,
+                              int32_t* __restrict__ pcol, T* __restrict__ pval,
+                              int32_t* __restrict__ prl, uint8_t* __restrict__ pidx) {
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= n_chunks) return;
+    bool lg;
+    const int len = packed_len(rl, cl, chunk_th, long_th, c, lane, &lg);
+    // rank in descending length, ties by row: a stable order
+    int rank = 0;
+    for (int o = 0; o < 32; ++o) {
+        const int lo = __shfl_sync(0xffffffffu, len, o);
+        rank += (lo > len) || (lo == len && o < lane);
+    }
+    prl[c * 32 + rank] = len;
+    pidx[c * 32 + rank] = (uint8_t)(lane | (lg ? 0x80 : 0));
+    const int maxlen = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+    int64_t pj = poff[c];
+    const int64_t src0 = cs[c] + lane;
+    for (int j = 0; j < maxlen; ++j) {
+        const int k = __popc(__ballot_sync(0xffffffffu, len > j));
+        if (j < len) {
+            pcol[pj + rank] = col[src0 + (int64_t)j * 32];
+            pval[pj + rank] = val[src0 + (int64_t)j * 32];
+        }
+        pj += k;
+    }
+}
+
+void free_packed(sellb_mat* m) {
+    cudaFree(m->poff);
+    cudaFree(m->pcol);
+    cudaFree(m->pval);
+    cudaFree(m->prl);
+    cudaFree(m->pidx);
+    m->poff = nullptr;
+    m->pcol = nullptr;
+    m->pval = nullptr;
+    m->prl = nullptr;
+    m->pidx = nullptr;
+    m->n_packed = 0;
+}
+
 }  // namespace
+
+namespace sellb {
+
+// force: 1 build, 0 drop, -1 cost model, -2 the build's default: off unless
+// SELLB_PACKED says 1 / auto (measured: the chunk-sorted kernel streams 2.1x
+// fewer bytes on cfg3 sigma=1 but is latency-bound at the same ~500 us as
+// the bulk role, so it is not the default yet -- DESIGN.md §4)
+int build_packed(sellb_mat* m, cudaStream_t st, int force) {
+    free_packed(m);
+    if (force == -2) {
+        const char* e = getenv("SELLB_PACKED");
+        force = !e ? 0 : (strcmp(e, "auto") == 0 ? -1 : (atoi(e) ? 1 : 0));
+    }
+    if (force == 0) return 0;
+    const bool possible = m->C == 32 && m->rl && m->n_chunks > 0 && m->slots > 0;
+    if (!possible) {
+        if (force == 1)
+            return set_error(SELLB_EPARAM, "the packed copy needs C = 32 and row_lengths");
+        return 0;
+    }
+    const int64_t vs = (int64_t)vsize(m->dtype);
+    DBuf d_cnt;
+    SELLB_CU(d_cnt.alloc((m->n_chunks + 1) * 8, st));
+    SELLB_CU(cudaMemsetAsync(d_cnt.p, 0, 8, st));
+    k_packed_count<<<(unsigned)grid_for(m->n_chunks * 32, 256), 256, 0, st>>>(
+        m->rl, m->cl, m->chunk_th, m->long_th, m->n_chunks, d_cnt.as<int64_t>() + 1);
+    if (int rc = check_stream_error()) return rc;
+    if (int rc = alloc_dev((void**)&m->poff, (m->n_chunks + 1) * 8)) return rc;
+    {
+        size_t tmp_bytes = 0;
+        SELLB_CU(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_cnt.as<int64_t>(), m->poff,
+                                               m->n_chunks + 1, st));
+        DBuf d_tmp;
+        SELLB_CU(d_tmp.alloc(tmp_bytes, st));
+        SELLB_CU(cub::DeviceScan::InclusiveSum(d_tmp.p, tmp_bytes, d_cnt.as<int64_t>(), m->poff,
+                                               m->n_chunks + 1, st));
+    }
+    int64_t total = 0;
+    SELLB_CU(cudaMemcpyAsync(&total, m->poff + m->n_chunks, 8, cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    if (force < 0) {
+        // cost model: the bytes the bulk role streams as configured (touched
+        // 32-byte sectors of the short rows' slots; the long rows read the
+        // side table either way) against the packed bytes + chunk offsets
+        if (m->variant != SELLB_VARIANT_PAD_SKIP) { free_packed(m); return 0; }
+        DBuf cnt;
+        SELLB_CU(cnt.alloc(4 * sizeof(unsigned long long), st));
+        SELLB_CU(cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned long long), st));
+        k_stream_count<<<(unsigned)grid_for(m->n_chunks, 256), 256, 0, st>>>(
+            m->rl, m->cl, m->chunk_th, m->n_chunks, m->C, 1, m->long_th, (int)vs,
+            cnt.as<unsigned long long>());
+        if (int rc = check_stream_error()) return rc;
+        unsigned long long h[4];
+        SELLB_CU(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+        double gain_min = 1.15;
+        if (const char* e = getenv("SELLB_PACKED_MIN_GAIN")) gain_min = atof(e);
+        const double skip_bytes = (double)h[2];     // 64-byte sectors (DRAM bursts)
+        const double packed_bytes = (double)(vs + 4) * (double)total + 8.0 * m->n_chunks;
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+        if (skip_bytes < gain_min * packed_bytes ||
+            (double)total * (double)(vs + 4) > 0.5 * (double)free_b) {
+            free_packed(m);
+            return 0;
+        }
+    }
+    if (int rc = alloc_dev((void**)&m->pcol, std::max<int64_t>(total, 1) * 4)) return rc;
+    if (int rc = alloc_dev(&m->pval, std::max<int64_t>(total, 1) * vs)) return rc;
+    if (int rc = alloc_dev((void**)&m->prl, m->n_pad * 4)) return rc;
+    if (int rc = alloc_dev((void**)&m->pidx, m->n_pad)) return rc;
+    const unsigned grid = (unsigned)grid_for(m->n_chunks * 32, 256);
+    if (m->dtype == SELLB_F32)
+        k_packed_fill<float><<<grid, 256, 0, st>>>(m->cs, m->cl, m->rl, m->col,
+                                                  (const float*)m->val, m->chunk_th, m->long_th,
+                                                  m->n_chunks, m->poff, m->pcol,
+                                                  (float*)m->pval, m->prl, m->pidx);
+    else
+        k_packed_fill<double><<<grid, 256, 0, st>>>(m->cs, m->cl, m->rl, m->col,
+                                                   (const double*)m->val, m->chunk_th,
+                                                   m->long_th, m->n_chunks, m->poff, m->pcol,
+                                                   (double*)m->pval, m->prl, m->pidx);
+    if (int rc = check_stream_error()) return rc;
+    SELLB_CU(cudaStreamSynchronize(st));
+    m->n_packed = total;
+    return 0;
+}
+
+}  // namespace sellb
 
 // ===========================================================================
 // ABI
@@ -768,6 +940,7 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     if (int rc = check_stream_error()) return rc;
     if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
     if (int rc = build_long_rows(m, st)) return rc;
+    if (int rc = build_packed(m, st, -2)) return rc;
     SELLB_CU(cudaStreamSynchronize(st));
     holder.m = nullptr;
     *out = m;
@@ -898,6 +1071,7 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
         m->variant = SELLB_VARIANT_AUTO;
         if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
         if (int rc = build_long_rows(m, st)) return rc;
+    if (int rc = build_packed(m, st, -2)) return rc;
     } else {
         m->nnz = -1;   // unknown without row_lengths
         m->variant = SELLB_VARIANT_PAD_INCL;
@@ -916,6 +1090,7 @@ int sellb_info(const sellb_mat* m, sellb_info_t* info) {
     info->slots = m->slots; info->nnz = m->nnz; info->dtype = m->dtype; info->device = m->device;
     info->col_permuted = m->col_permuted; info->variant = m->variant;
     info->has_row_lengths = m->rl != nullptr; info->max_cl = m->max_cl;
+    info->packed = m->pcol != nullptr;
     return 0;
 }
 
@@ -1021,6 +1196,7 @@ int sellb_infer_row_lengths(sellb_mat* m, void* stream) {
     m->variant = SELLB_VARIANT_AUTO;
     if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
     if (int rc = build_long_rows(m, st)) return rc;
+    if (int rc = build_packed(m, st, -2)) return rc;
     return 0;
 }
 
@@ -1035,6 +1211,14 @@ int sellb_set_variant(sellb_mat* m, int32_t variant) {
     m->variant = variant;
     if (variant == SELLB_VARIANT_AUTO) return choose_variant(m, 0, nullptr, nullptr, nullptr);
     return 0;
+}
+
+int sellb_set_packed(sellb_mat* m, int32_t mode) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    if (mode < -1 || mode > 1) return set_error(SELLB_EPARAM, "packed mode must be -1, 0 or 1");
+    DeviceGuard guard(m->device);
+    return build_packed(m, 0, mode);
 }
 
 void sellb_free(sellb_mat* m) {

@@ -58,6 +58,21 @@ struct sellb_mat {
     int64_t* side_off = nullptr;
     int32_t* side_col = nullptr;
     void* side_val = nullptr;
+    // chunk-sorted packed copy (sellb_build.cu build_packed, kernel
+    // k_spmv_packed; the pJDS idea inside each C = 32 chunk): the chunk's
+    // short rows re-ordered by descending length, stored slot-major without
+    // padding -- slot j holds the k_j rows longer than j, contiguous, and
+    // slot j+1 follows it -- so the warp streams each chunk as one dense run.
+    // prl / pidx: the sorted rows' lengths and their row within the chunk
+    // (bit 7: a long row, summed by the warp-per-row role).  The SELL arrays
+    // stay the exported layout; the copy only changes which bytes the SpMV
+    // streams.
+    int64_t* poff = nullptr;          // n_chunks + 1 packed chunk offsets
+    int32_t* pcol = nullptr;
+    void* pval = nullptr;
+    int32_t* prl = nullptr;           // n_pad
+    uint8_t* pidx = nullptr;          // n_pad
+    int64_t n_packed = 0;
     int32_t long_th = 0x7fffffff;     // chunks wider than this may hold long rows
     int32_t* chunk_th = nullptr;      // per chunk: rows longer than this are long
     // long-row kernel on a side stream, forked from / joined into the
@@ -159,6 +174,8 @@ bool long_tma_possible(const sellb_mat* m);
 void host_parallel_copy(void* dst, const void* src, size_t n);
 bool is_pinned(const void* p);
 int ensure_host_mirror(void** slot, size_t bytes);
+
+int build_packed(sellb_mat* m, cudaStream_t st, int force);
 
 inline int64_t grid_for(int64_t n, int threads) { return (n + threads - 1) / threads; }
 

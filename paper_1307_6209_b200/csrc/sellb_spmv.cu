@@ -700,6 +700,105 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
 }
 
+// Chunk-sorted packed kernel (C = 32, pad-heavy layouts; sellb_build.cu
+// build_packed): one warp per chunk, one thread per row as in the bulk role,
+// but the rows of the chunk come sorted by descending length and stored
+// slot-major without padding -- the k_j rows longer than slot j occupy lanes
+// 0..k_j-1 and k_j consecutive elements, slot j+1 follows.  k_j is one warp
+// vote, so a warp walks the chunk as one dense, fully coalesced run: the
+// bytes streamed are (s_v + 4) per nonzero instead of every 32-byte sector
+// with an active lane.  Each thread still sums its own row from +0.0 in slot
+// order (U-slot batches: loads, then gathers, then the ordered adds) and
+// stores it to its original row, so y is bitwise the reference's.  Long
+// rows (the bulk role's rule) take the warp-per-row role of blocks
+// [0, n_long_blocks), reading the side table.
+template <typename T, bool ACC, int ORD, int U>
+__global__ void __launch_bounds__(kThreads, U == 8 ? 4 : 6)
+k_spmv_packed(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+              const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+              const T* __restrict__ val, const int64_t* __restrict__ poff,
+              const int32_t* __restrict__ pcol, const T* __restrict__ pval,
+              const int32_t* __restrict__ prl, const uint8_t* __restrict__ pidx,
+              const T* __restrict__ x, T* __restrict__ y, const int32_t* __restrict__ order,
+              int64_t c0, int64_t c1, int64_t n_rows, const int32_t* __restrict__ long_rows,
+              int64_t n_long, int l2pol, const int64_t* __restrict__ side_off,
+              const int32_t* __restrict__ side_col, const T* __restrict__ side_val) {
+    constexpr int WPB = kThreads / 32;
+    const uint64_t pol_s = make_policy(l2pol & 0xf);
+    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n_long_blocks = (n_long + WPB - 1) / WPB;
+    if ((int64_t)blockIdx.x < n_long_blocks) {       // long-row role
+        __shared__ T stage[WPB][kSeg * 32];
+        const int64_t k = (int64_t)blockIdx.x * WPB + warp;
+        if (k >= n_long) return;
+        const int64_t p = long_rows[k];
+        if (p < c0 * 32 || p >= c1 * 32) return;
+        const int64_t chunk = p >> 5;
+        if (side_off) {
+            const int64_t o = side_off[k];
+            long_row_at<T, ACC, ORD>(side_val + o, side_col + o, 1, rl[p], cl[chunk], x, y,
+                                     order, p, n_rows, lane, pol_s, pol_x, stage[warp]);
+        } else {
+            const int64_t base = cs[chunk] + (p - chunk * 32);
+            long_row_at<T, ACC, ORD>(val + base, col + base, 32, rl[p], cl[chunk], x, y, order,
+                                     p, n_rows, lane, pol_s, pol_x, stage[warp]);
+        }
+        return;
+    }
+    const int64_t c = c0 + ((int64_t)blockIdx.x - n_long_blocks) * WPB + warp;
+    if (c >= c1) return;
+    const int len = prl[c * 32 + lane];
+    const int tag = pidx[c * 32 + lane];
+    const int maxlen = __shfl_sync(0xffffffffu, len, 0);       // lane 0: the longest row
+    const bool vx = (l2pol >> 8) & 1;
+    const int64_t cbase = poff[c];
+    const T* __restrict__ pv = pval + cbase;
+    const int32_t* __restrict__ pc = pcol + cbase;
+    int pj = 0;                                   // a chunk's packed run is < 2^31 entries
+    T sum = T(0);
+    for (int j = 0; j < maxlen; j += U) {
+        int off[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            off[u] = pj + lane;
+            pj += __popc(__ballot_sync(0xffffffffu, len > j + u));
+        }
+        T v[U];
+        int32_t ci[U];
+        T xv[U];
+        if (j + U <= len) {                       // a full batch
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                v[u] = ld_stream(pv + off[u], pol_s);
+                ci[u] = ld_stream(pc + off[u], pol_s);
+            }
+            gather_x<T, U>(xv, ci, x, pol_x, vx);
+#pragma unroll
+            for (int u = 0; u < U; ++u) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
+        } else if (j < len) {                     // this row's tail
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                v[u] = T(0);
+                ci[u] = 0;
+                if (j + u < len) {
+                    v[u] = ld_stream(pv + off[u], pol_s);
+                    ci[u] = ld_stream(pc + off[u], pol_s);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = (j + u < len) ? ld_x(x + ci[u], pol_x) : T(0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (j + u < len) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
+        }
+    }
+    if (tag & 0x80) return;                                     // stored by the long-row role
+    const int64_t p = c * 32 + (tag & 31);
+    if (len < cl[c]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+    store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
+}
+
 // Persistent "short chunk" variant (C = 32, no long rows): a grid of a few
 // blocks per SM whose warps sweep chunks c, c + n_warps, ...; the next
 // chunk's metadata (cs, cl, row length) is fetched before the current chunk
@@ -1253,10 +1352,54 @@ int dispatch_acc(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t
                : dispatch_u<T, CC, SKIP, false, 0>(m, x, y, p0, p1, st);
 }
 
+template <typename T, bool ACC, int ORD>
+int launch_packed(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
+                  cudaStream_t st) {
+    static const int l2pol_env = [] {
+        const char* e = getenv("SELLB_L2POL");
+        return e ? (int)strtol(e, nullptr, 0) : -1;
+    }();
+    static const int vx_env = [] {
+        const char* e = getenv("SELLB_VX");
+        return e ? atoi(e) : 1;
+    }();
+    const int vx = (vx_env && ((uintptr_t)x & 15) == 0) ? 0x100 : 0;
+    const int l2pol = (l2pol_env >= 0 ? l2pol_env
+                       : ((int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20))
+                      | vx;
+    const int64_t n_long = m->long_rows ? m->n_long : 0;
+    const bool side = m->side_off && m->n_rest == n_long && !m->n_groups;
+    const int32_t* lr = side ? m->long_rest : m->long_rows;
+    const int64_t wpb = kThreads / 32;
+    const unsigned grid = (unsigned)((n_long + wpb - 1) / wpb + (c1 - c0 + wpb - 1) / wpb);
+    static const int u_env = [] {
+        const char* e = getenv("SELLB_PACKED_U");
+        return e ? atoi(e) : 8;
+    }();
+#define SELLB_PK(UU)                                                                          \
+    k_spmv_packed<T, ACC, ORD, UU><<<grid, kThreads, 0, st>>>(                                \
+        m->cs, m->cl, m->rl, m->col, (const T*)m->val, m->poff, m->pcol, (const T*)m->pval,   \
+        m->prl, m->pidx, (const T*)x, (T*)y, m->order, c0, c1, m->n_rows, lr, n_long, l2pol,  \
+        side ? m->side_off : nullptr, side ? m->side_col : nullptr,                           \
+        (const T*)(side ? m->side_val : nullptr))
+    if (u_env == 4) SELLB_PK(4);
+    else SELLB_PK(8);
+#undef SELLB_PK
+    count_launches();
+    return 0;
+}
+
 template <typename T>
 int dispatch_sell(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1, int acc,
                   int ord, cudaStream_t st) {
     const bool skip = m->variant == SELLB_VARIANT_PAD_SKIP && m->rl;
+    if (skip && m->pcol && m->C == 32 && !m->n_groups) {
+        const int64_t c0 = p0 / 32, c1 = p1 / 32;
+        if (acc) return ord ? launch_packed<T, true, 1>(m, x, y, c0, c1, st)
+                            : launch_packed<T, true, 0>(m, x, y, c0, c1, st);
+        return ord ? launch_packed<T, false, 1>(m, x, y, c0, c1, st)
+                   : launch_packed<T, false, 0>(m, x, y, c0, c1, st);
+    }
     if (m->C == 32) {
         return skip ? dispatch_acc<T, 32, true>(m, x, y, p0, p1, acc, ord, st)
                     : dispatch_acc<T, 32, false>(m, x, y, p0, p1, acc, ord, st);

@@ -96,7 +96,12 @@ class HaloPlan:
 
     ``recv[p]``: sorted global indices this rank needs from rank p;
     ``send[p]``: sorted global indices (owned here) rank p needs from us.
-    Built with one all_gather of the request lists (setup only)."""
+    Built with one all_gather of the request lists (setup only).
+
+    x[0] is never part of a halo: rank 0 sends it on its own to every rank
+    that reads it (a real column-0 entry, or the reference's 0*x[0] padding
+    term), into a separate one-element buffer, so no receive ever writes
+    x_full[0] while the interior chunks may read it (DistSpmv.step)."""
 
     def __init__(self, rank, world, bounds, recv, send, need_x0):
         self.rank, self.world = rank, world
@@ -112,13 +117,20 @@ class HaloPlan:
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
         col = np.asarray(col_local)
         remote = np.unique(col[(col < r0) | (col >= r1)]).astype(np.int64)
+        remote = remote[remote != 0]                 # x[0] travels separately
         owner = np.searchsorted(bounds, remote, side="right") - 1
         return {int(p): remote[owner == p].astype(np.int32)
                 for p in np.unique(owner) if p != rank}
 
+    @staticmethod
+    def reads_x0(col_local, bounds, rank):
+        """Whether this rank's block has a real entry in (non-owned) column 0."""
+        return rank != 0 and int(bounds[rank]) > 0 and bool(np.any(np.asarray(col_local) == 0))
+
     @classmethod
     def from_requests(cls, rank, world, bounds, gathered):
-        """gathered[p] = (requests of rank p, rank p has padding)."""
+        """gathered[p] = (requests of rank p, rank p has padding[, rank p reads
+        column 0 as a real entry])."""
         recv = gathered[rank][0]
         send = {}
         for p in range(world):
@@ -127,14 +139,17 @@ class HaloPlan:
             want = gathered[p][0].get(rank)
             if want is not None and len(want):
                 send[p] = np.asarray(want, dtype=np.int32)
-        need_x0 = {p: bool(gathered[p][1]) and p != 0 for p in range(world)}
+        need_x0 = {p: p != 0 and (bool(gathered[p][1]) or
+                                  (len(gathered[p]) > 2 and bool(gathered[p][2])))
+                   for p in range(world)}
         return cls(rank, world, bounds, recv, send, need_x0)
 
     @classmethod
     def build(cls, col_local, bounds, rank, world, has_padding, group=None):
         recv = cls.requests(col_local, bounds, rank)
         gathered = [None] * world
-        tdist.all_gather_object(gathered, (recv, bool(has_padding)), group=group)
+        tdist.all_gather_object(gathered, (recv, bool(has_padding),
+                                           cls.reads_x0(col_local, bounds, rank)), group=group)
         return cls.from_requests(rank, world, bounds, gathered)
 
     def halo_entries(self):
@@ -296,9 +311,16 @@ class DistSpmv:
         fix-up -- in a CUDA graph so later steps cost one replay of host
         time instead of ~40-90 us of NCCL post per step
         (profiles/r01f_p2p_overhead.txt).  Collective: every rank must call
-        it.  The graph is kept only if its replay reproduces the eager y
-        bitwise on EVERY rank (MIN-reduced flag); otherwise all ranks stay
-        eager.  Returns whether the graph is in use."""
+        it.  The graph is kept only if its replay -- with every halo entry,
+        receive buffer and x[0] poisoned with NaN beforehand -- reproduces the
+        eager y bitwise on EVERY rank (MIN-reduced flag); otherwise all ranks
+        stay eager.  Returns whether the graph is in use.
+
+        Known limit: if the capture fails on one rank after its P2P batch was
+        recorded and not on another, the ranks' NCCL P2P sequences may no
+        longer match and the eager fallback step can hang; the bench leg
+        therefore keeps the graph opt-in (SELLB_DIST_GRAPH=1) and the
+        multi-rank tests run under a timeout."""
         if self.device.type != "cuda":
             return False
         def all_ok(v):
@@ -332,6 +354,15 @@ class DistSpmv:
             ok = 1.0
             try:
                 self.y.zero_()
+                # poison everything the exchange must deliver: a replay whose
+                # receives land nothing cannot reproduce y_ref
+                self.x_full[:self.r0].fill_(float("nan"))
+                self.x_full[self.r1:].fill_(float("nan"))
+                self.x0_buf.fill_(float("nan"))
+                for _, buf, gidx in self.recv_ops:
+                    if gidx is not None:
+                        buf.fill_(float("nan"))
+                torch.cuda.synchronize(self.device)
                 dbg("replaying")
                 g.replay()
                 torch.cuda.synchronize(self.device)
@@ -359,10 +390,18 @@ class DistSpmv:
             self.graph = None
 
     def _step_eager(self):
+        if self.x0_recv:
+            # the interior chunks may read x_full[0] (padding: 0 * x[0]); it
+            # holds +0.0 until the exchange has landed, so a previous step's
+            # non-finite x[0] cannot leak into them -- the fix-up below adds
+            # 0 * x[0] for the current one
+            self.x_full[0:1].zero_()
         works = self._post_exchange()
         self.engine.run_ranges(self.interior, self.x_full, self.y)
         for w in works:
             w.wait()
+        if self.x0_recv:
+            self.x_full[0:1].copy_(self.x0_buf)
         for p, buf, gidx in self.recv_ops:
             if gidx is not None:
                 self.engine.scatter(buf, gidx, self.x_full)
@@ -396,6 +435,7 @@ def requests_torch(col_t, bounds, rank):
     matrix lives (torch.unique / searchsorted on the GPU)."""
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     remote = torch.unique(col_t[(col_t < r0) | (col_t >= r1)])
+    remote = remote[remote != 0]                     # x[0] travels separately
     if remote.numel() == 0:
         return {}
     b = torch.as_tensor(np.asarray(bounds, dtype=np.int64), device=col_t.device)
@@ -423,8 +463,9 @@ def setup_device(rpt_t, col_t, val_t, n_global, bounds, C, sigma, rank, world, d
     has_padding = info.slots > info.nnz
     if gathered is None:
         plan_req = requests_torch(col_t, bounds, rank)
+        reads0 = rank != 0 and int(bounds[rank]) > 0 and bool((col_t == 0).any().item())
         gathered = [None] * world
-        tdist.all_gather_object(gathered, (plan_req, bool(has_padding)), group=group)
+        tdist.all_gather_object(gathered, (plan_req, bool(has_padding), reads0), group=group)
     plan = HaloPlan.from_requests(rank, world, bounds, gathered)
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     remote = ((col_t < r0) | (col_t >= r1)).to(torch.int64)

@@ -454,6 +454,18 @@ class SellMatrix:
     def variant(self):
         return {1: "pad_skip", 2: "pad_incl"}.get(self.info().variant, "auto")
 
+    @property
+    def packed(self):
+        """Whether the SpMV streams the packed chunk copy (pad-heavy C = 32
+        layouts; the exported SELL arrays are unchanged)."""
+        return bool(self.info().packed)
+
+    def set_packed(self, mode):
+        """True builds the packed chunk copy, False drops it, None lets the
+        build's cost model decide (sellb_set_packed)."""
+        code = -1 if mode is None else (1 if mode else 0)
+        _lib.check(_lib.load().sellb_set_packed(self.handle, code))
+
     def set_variant(self, name):
         code = {"auto": _lib.VARIANT_AUTO, "pad_skip": _lib.VARIANT_PAD_SKIP,
                 "pad_incl": _lib.VARIANT_PAD_INCL}.get(name)

@@ -80,12 +80,16 @@ def _worker(rank, world, port, case, C, sigma, q):
         tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
                                  rank=rank, world_size=world)
         m = case()
-        bounds = dist.partition_rows(m.rpt, world, C, sigma)
+        bounds = (dist._cfg5_bounds(m.n_rows, world, C, sigma) if case is case_cfg5
+                  else dist.partition_rows(m.rpt, world, C, sigma))
         loc = block(m, int(bounds[rank]), int(bounds[rank + 1]))
         ds = dist.setup(loc, bounds, C, sigma, rank, world, torch.device("cpu"),
                         oracle_factory(C, sigma))
         out = {}
-        for tag, x0 in (("finite", None), ("inf", np.inf)):
+        # the order matters: a finite x[0] right after a non-finite one must
+        # not inherit it (x[0] travels apart from the halo)
+        for tag, x0 in (("finite", None), ("inf", np.inf), ("finite_after_inf", None),
+                        ("nan", np.nan), ("finite_after_nan", None)):
             x = generate.rhs(m.n_cols)
             if x0 is not None:
                 x[0] = x0
@@ -135,6 +139,30 @@ def case_powerlaw():
     return generate.powerlaw(4000, seed=9, band=300)
 
 
+def case_arrow():
+    """Banded plus real entries in column 0 on every 7th row: ranks other
+    than 0 read x[0] as a matrix entry, not only as padding."""
+    m = banded(2003, 6)
+    rows = np.arange(m.n_rows)
+    extra = rows[(rows % 7 == 3)]
+    rr = np.concatenate([np.repeat(rows, np.diff(m.rpt)), extra])
+    cc = np.concatenate([m.col, np.zeros(len(extra), dtype=m.col.dtype)])
+    vv = np.concatenate([m.val, np.full(len(extra), 0.5)])
+    key = rr * m.n_cols + cc
+    key, first = np.unique(key, return_index=True)
+    rr, cc, vv = key // m.n_cols, key % m.n_cols, vv[first]
+    rpt = np.zeros(m.n_rows + 1, np.int64)
+    np.cumsum(np.bincount(rr, minlength=m.n_rows), out=rpt[1:])
+    return CRSMatrix(m.n_rows, m.n_cols, rpt, cc.astype(np.int32), vv)
+
+
+def case_cfg5():
+    """The cfg5 generator's structure (hopping offsets up to +-2^20 scaled
+    down: N = 2^16, so the +-4096 / +-65536 hops cross every rank) in the
+    strong-scaling layout: _cfg5_bounds, SELL-32-512."""
+    return generate.hamiltonian(1 << 16)
+
+
 def single(m, C, sigma, x):
     o = oracle.crs_to_sell(m.rpt, m.col, m.val, m.n_rows, m.n_cols, C, sigma)
     with np.errstate(invalid="ignore"):
@@ -143,12 +171,24 @@ def single(m, C, sigma, x):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("case,C,sigma", [(case_banded, 32, 1), (case_banded, 8, 64),
-                                          (case_stencil, 32, 1), (case_powerlaw, 32, 128)])
+                                          (case_stencil, 32, 1), (case_powerlaw, 32, 128),
+                                          (case_arrow, 32, 1)])
 def test_distributed_equals_single(world, case, C, sigma):
+    check_world(world, case, C, sigma)
+
+
+def test_cfg5_layout_world4():
+    """World 4 over gloo on the cfg5 strong-scaling layout (oracle engine)."""
+    check_world(4, case_cfg5, 32, 512)
+
+
+def check_world(world, case, C, sigma):
     m = case()
-    bounds = dist.partition_rows(m.rpt, world, C, sigma)
+    bounds = (dist._cfg5_bounds(m.n_rows, world, C, sigma) if case is case_cfg5
+              else dist.partition_rows(m.rpt, world, C, sigma))
     res = run_world(world, case, C, sigma)
-    for tag, x0 in (("finite", None), ("inf", np.inf)):
+    for tag, x0 in (("finite", None), ("inf", np.inf), ("finite_after_inf", None),
+                    ("nan", np.nan), ("finite_after_nan", None)):
         x = generate.rhs(m.n_cols)
         if x0 is not None:
             x[0] = x0
@@ -156,13 +196,13 @@ def test_distributed_equals_single(world, case, C, sigma):
             r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
             # block-decomposition: the block's own build equals the global slice
             _, y_ref = single(block(m, r0, r1), C, sigma, x)
-            if tag == "finite":
+            if x0 is None:
                 assert out[tag].tobytes() == y_ref.tobytes(), (rank, tag)
             else:
                 np.testing.assert_array_equal(out[tag], y_ref)
         # and the stitched result equals the single-GPU product (stored order
         # of each block = global stored order when boundaries are lcm-aligned)
-        if tag == "finite":
+        if x0 is None:
             o_all, y_all = single(m, C, sigma, x)
             stitched = np.concatenate([r[1][tag][: int(bounds[r[0] + 1] - bounds[r[0]])]
                                        for r in res])

@@ -30,8 +30,8 @@ def virtual_cluster(m, world, C, sigma):
     blocks = [block(m, int(bounds[r]), int(bounds[r + 1])) for r in range(world)]
     make = dist.cuda_engine_factory(C, sigma, dev)
     built = [make(b) for b in blocks]
-    gathered = [(dist.HaloPlan.requests(b.col, bounds, r), built[r][1]["has_padding"])
-                for r, b in enumerate(blocks)]
+    gathered = [(dist.HaloPlan.requests(b.col, bounds, r), built[r][1]["has_padding"],
+                 dist.HaloPlan.reads_x0(b.col, bounds, r)) for r, b in enumerate(blocks)]
     dss = [dist.setup(b, bounds, C, sigma, r, world, dev, None,
                       plan=dist.HaloPlan.from_requests(r, world, bounds, gathered),
                       built=built[r]) for r, b in enumerate(blocks)]
@@ -39,9 +39,12 @@ def virtual_cluster(m, world, C, sigma):
 
 
 def loopback_step(dss, x):
+    """DistSpmv._step_eager with the NCCL batch replaced by device copies."""
     xt = torch.from_numpy(x).cuda()
     for ds in dss:
         ds.x_local.copy_(xt[ds.r0:ds.r1])
+        if ds.x0_recv:
+            ds.x_full[0:1].zero_()
     for r, ds in enumerate(dss):
         for p, buf, gidx in ds.send_ops:
             if gidx is not None:
@@ -52,6 +55,8 @@ def loopback_step(dss, x):
             dss[p].x0_buf.copy_(ds.x_full[0:1])
     for ds in dss:
         ds.engine.run_ranges(ds.interior, ds.x_full, ds.y)
+        if ds.x0_recv:
+            ds.x_full[0:1].copy_(ds.x0_buf)
         for p, buf, gidx in ds.recv_ops:
             if gidx is not None:
                 ds.engine.scatter(buf, gidx, ds.x_full)
@@ -98,7 +103,8 @@ def test_cfg5_device_setup_loopback():
     bounds = dist._cfg5_bounds(n, world, C, sigma)
     blocks = [generate.hamiltonian_device(n, int(bounds[r]), int(bounds[r + 1]))
               for r in range(world)]
-    gathered = [(dist.requests_torch(b[1], bounds, r), True) for r, b in enumerate(blocks)]
+    gathered = [(dist.requests_torch(b[1], bounds, r), True,
+                 r > 0 and bool((b[1] == 0).any().item())) for r, b in enumerate(blocks)]
     dss = [dist.setup_device(b[0], b[1], b[2], n, bounds, C, sigma, r, world, dev,
                              gathered=gathered) for r, b in enumerate(blocks)]
     rpt, col, val = generate.hamiltonian_device(n)

@@ -255,8 +255,10 @@ _CFG4 = {}
 
 
 def _cfg4():
+    """BASELINE configs[3] at the size bench.py measures: gen_skewed(2^21,
+    base 8, 1024 spikes of 2048) (the reference's generate.py:72-96)."""
     if "m" not in _CFG4:
-        _CFG4["m"] = sb.coo_to_crs(sb.gen_skewed(1 << 20, 8, 2048, 512))
+        _CFG4["m"] = sb.coo_to_crs(sb.gen_skewed(1 << 21, 8, 2048, 1024))
     return _CFG4["m"]
 
 
