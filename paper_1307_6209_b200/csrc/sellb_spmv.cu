@@ -701,19 +701,29 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
 }
 
 // Chunk-sorted packed kernel (C = 32, pad-heavy layouts; sellb_build.cu
-// build_packed): one warp per chunk, one thread per row as in the bulk role,
-// but the rows of the chunk come sorted by descending length and stored
-// slot-major without padding -- the k_j rows longer than slot j occupy lanes
-// 0..k_j-1 and k_j consecutive elements, slot j+1 follows.  k_j is one warp
-// vote, so a warp walks the chunk as one dense, fully coalesced run: the
-// bytes streamed are (s_v + 4) per nonzero instead of every 32-byte sector
-// with an active lane.  Each thread still sums its own row from +0.0 in slot
-// order (U-slot batches: loads, then gathers, then the ordered adds) and
-// stores it to its original row, so y is bitwise the reference's.  Long
-// rows (the bulk role's rule) take the warp-per-row role of blocks
+// build_packed).  The chunk's rows come sorted by descending length and
+// stored slot-major without padding: slot j holds the k_j rows longer than
+// j as k_j consecutive entries (row r of slot j at P_j + r), slot j+1
+// follows.  One warp per chunk streams the run in tiles of E = 32 U
+// entries:
+//   phase 1 -- lane t takes entries t, t+32, ... of the tile: dense,
+//              coalesced val/col loads (every lane busy whatever the row
+//              lengths), the x gathers, the rounded products into the warp's
+//              shared-memory stage; the next tile's val/col loads are issued
+//              before this tile's gathers are consumed (one round trip in
+//              flight behind the other);
+//   phase 2 -- lane r (the r-th longest row) walks its own entries P_j + r
+//              that fall in the tile, in slot order, adding them to its sum.
+//              P_{j+1} = P_j + k_j, and k_j (rows longer than j) follows from
+//              the chunk's sorted lengths kept in shared memory -- no warp
+//              vote per slot.
+// So the bytes streamed are (s_v + 4) per nonzero and the memory
+// instructions are dense, while each row is still summed from +0.0 in slot
+// order with separately rounded products: y is bitwise the reference's.
+// Long rows (the bulk role's rule) take the warp-per-row role of blocks
 // [0, n_long_blocks), reading the side table.
 template <typename T, bool ACC, int ORD, int U>
-__global__ void __launch_bounds__(kThreads, U == 8 ? 4 : 6)
+__global__ void __launch_bounds__(kThreads, U >= 8 ? 3 : 4)
 k_spmv_packed(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
               const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
               const T* __restrict__ val, const int64_t* __restrict__ poff,
@@ -724,12 +734,16 @@ k_spmv_packed(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
               int64_t n_long, int l2pol, const int64_t* __restrict__ side_off,
               const int32_t* __restrict__ side_col, const T* __restrict__ side_val) {
     constexpr int WPB = kThreads / 32;
+    constexpr int E = 32 * U;                         // entries per tile
+    static_assert(E >= kSeg * 32, "stage too small for the long-row role");
+    __shared__ __align__(16) T stage[WPB][E];
+    __shared__ int slens[WPB][32];
     const uint64_t pol_s = make_policy(l2pol & 0xf);
     const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* st = stage[warp];
     const int64_t n_long_blocks = (n_long + WPB - 1) / WPB;
     if ((int64_t)blockIdx.x < n_long_blocks) {       // long-row role
-        __shared__ T stage[WPB][kSeg * 32];
         const int64_t k = (int64_t)blockIdx.x * WPB + warp;
         if (k >= n_long) return;
         const int64_t p = long_rows[k];
@@ -738,11 +752,11 @@ k_spmv_packed(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
         if (side_off) {
             const int64_t o = side_off[k];
             long_row_at<T, ACC, ORD>(side_val + o, side_col + o, 1, rl[p], cl[chunk], x, y,
-                                     order, p, n_rows, lane, pol_s, pol_x, stage[warp]);
+                                     order, p, n_rows, lane, pol_s, pol_x, st);
         } else {
             const int64_t base = cs[chunk] + (p - chunk * 32);
             long_row_at<T, ACC, ORD>(val + base, col + base, 32, rl[p], cl[chunk], x, y, order,
-                                     p, n_rows, lane, pol_s, pol_x, stage[warp]);
+                                     p, n_rows, lane, pol_s, pol_x, st);
         }
         return;
     }
@@ -750,47 +764,62 @@ k_spmv_packed(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     if (c >= c1) return;
     const int len = prl[c * 32 + lane];
     const int tag = pidx[c * 32 + lane];
-    const int maxlen = __shfl_sync(0xffffffffu, len, 0);       // lane 0: the longest row
-    const bool vx = (l2pol >> 8) & 1;
+    slens[warp][lane] = len;
     const int64_t cbase = poff[c];
+    const int tot = (int)(poff[c + 1] - cbase);
     const T* __restrict__ pv = pval + cbase;
     const int32_t* __restrict__ pc = pcol + cbase;
-    int pj = 0;                                   // a chunk's packed run is < 2^31 entries
+    // this lane's walk: next slot jl, its entry offset Pl + lane, k = k_jl
+    int jl = 0, Pl = 0;
+    int kc = __popc(__ballot_sync(0xffffffffu, len > 0));
+    __syncwarp();
     T sum = T(0);
-    for (int j = 0; j < maxlen; j += U) {
-        int off[U];
+    T v[U];
+    int32_t ci[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int t = u * 32 + lane;
+        v[u] = T(0);
+        ci[u] = 0;
+        if (t < tot) {
+            v[u] = ld_stream(pv + t, pol_s);
+            ci[u] = ld_stream(pc + t, pol_s);
+        }
+    }
+    for (int tb = 0; tb < tot; tb += E) {
+        T xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = (tb + u * 32 + lane < tot) ? ld_x(x + ci[u], pol_x) : T(0);
+        // the next tile's matrix entries, in flight behind this tile's gathers
+        T vn[U];
+        int32_t cn[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            off[u] = pj + lane;
-            pj += __popc(__ballot_sync(0xffffffffu, len > j + u));
+            const int t = tb + E + u * 32 + lane;
+            vn[u] = T(0);
+            cn[u] = 0;
+            if (t < tot) {
+                vn[u] = ld_stream(pv + t, pol_s);
+                cn[u] = ld_stream(pc + t, pol_s);
+            }
         }
-        T v[U];
-        int32_t ci[U];
-        T xv[U];
-        if (j + U <= len) {                       // a full batch
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                v[u] = ld_stream(pv + off[u], pol_s);
-                ci[u] = ld_stream(pc + off[u], pol_s);
-            }
-            gather_x<T, U>(xv, ci, x, pol_x, vx);
+        for (int u = 0; u < U; ++u)
+            if (tb + u * 32 + lane < tot) st[u * 32 + lane] = Arith<T>::mul(v[u], xv[u]);
+        __syncwarp();
+        // phase 2: this row's entries inside [tb, tb + E), in slot order
+        const int te = tb + E;
+        while (jl < len && Pl + lane < te) {
+            sum = Arith<T>::add(sum, st[Pl + lane - tb]);
+            Pl += kc;
+            ++jl;
+            while (kc > 0 && slens[warp][kc - 1] <= jl) --kc;
+        }
+        __syncwarp();
 #pragma unroll
-            for (int u = 0; u < U; ++u) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
-        } else if (j < len) {                     // this row's tail
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                v[u] = T(0);
-                ci[u] = 0;
-                if (j + u < len) {
-                    v[u] = ld_stream(pv + off[u], pol_s);
-                    ci[u] = ld_stream(pc + off[u], pol_s);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = (j + u < len) ? ld_x(x + ci[u], pol_x) : T(0);
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (j + u < len) sum = Arith<T>::add(sum, Arith<T>::mul(v[u], xv[u]));
+        for (int u = 0; u < U; ++u) {
+            v[u] = vn[u];
+            ci[u] = cn[u];
         }
     }
     if (tag & 0x80) return;                                     // stored by the long-row role
@@ -1328,8 +1357,10 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         // side table applies unless the fused warp-per-row role is forced
         const bool side = long_mode != 0 && m->side_off && m->n_rest == n_long;
         const int32_t* lr = side ? m->long_rest : m->long_rows;
-        if (u8) SELLB_LAUNCH(8, true, lr, n_long, m->long_th, side);
-        else SELLB_LAUNCH(4, true, lr, n_long, m->long_th, side);
+        static const bool no_long = getenv("SELLB_TIME_NO_LONG") && atoi(getenv("SELLB_TIME_NO_LONG"));
+        const int64_t nl = no_long ? 0 : n_long;      // timing experiments only
+        if (u8) SELLB_LAUNCH(8, true, lr, nl, m->long_th, side);
+        else SELLB_LAUNCH(4, true, lr, nl, m->long_th, side);
     } else if (u_env == 6 || (!u_env && m->max_cl > 4 && m->max_cl <= 6 && sizeof(T) == 8)) {
         // every chunk fits one 6-slot batch (5-point stencils): one round trip
         SELLB_LAUNCH(6, false, nullptr, 0, 0x7fffffff, false);
@@ -1367,7 +1398,10 @@ int launch_packed(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_
     const int l2pol = (l2pol_env >= 0 ? l2pol_env
                        : ((int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20))
                       | vx;
-    const int64_t n_long = m->long_rows ? m->n_long : 0;
+    // SELLB_TIME_NO_LONG=1: timing experiments only -- the long rows are
+    // not summed (y wrong for them), isolating the packed role's time
+    static const bool no_long = getenv("SELLB_TIME_NO_LONG") && atoi(getenv("SELLB_TIME_NO_LONG"));
+    const int64_t n_long = (m->long_rows && !no_long) ? m->n_long : 0;
     const bool side = m->side_off && m->n_rest == n_long && !m->n_groups;
     const int32_t* lr = side ? m->long_rest : m->long_rows;
     const int64_t wpb = kThreads / 32;

@@ -8,7 +8,7 @@ for cs in ${CFGS:-cfg3:1 cfg3:128 cfg3:512 cfg3:4000000 cfg4:1 cfg4:512 cfg1:1 c
   for pk in ${PKS:-0 auto}; do
     if [ $pk = auto ]; then unset SELLB_PACKED; else export SELLB_PACKED=$pk; fi
     out=gpurun_out/packed_ab/${cfg}_s${sig}_pk${pk}${TAG}
-    python bench.py --config $cfg --sigma $sig --steps ${STEPS:-200} --warmup 10 --skip-cpu \
+    python bench.py --config $cfg --sigma $sig --steps ${STEPS:-200} --warmup 10 --skip-cpu $BENCH_EXTRA \
       > $out.json 2> $out.err
     python - "$out.json" "$cfg" "$sig" "$pk$TAG" <<'PY'
 import json, sys
