@@ -155,12 +155,12 @@ int sellb_infer_row_lengths(sellb_mat* m, void* stream);
 
 int sellb_set_variant(sellb_mat* m, int32_t variant);
 
-/* Chunk-sorted packed copy for pad-heavy C = 32 layouts: 1 builds it (the
- * SpMV then streams every short row's entries without padding, bit-identical
- * sums), 0 drops it, -1 applies the cost model (packed when the pad-skipping
- * kernel's touched 64-byte sectors exceed the packed bytes by more than
- * SELLB_PACKED_MIN_GAIN, default 1.15).  Builds leave it off unless the
- * environment sets SELLB_PACKED=1 or SELLB_PACKED=auto. */
+/* Packed stored-order copy for pad-heavy C = 32 layouts: 1 builds it (the
+ * SpMV then streams every row's entries without padding through the
+ * row-run kernel, bit-identical sums), 0 drops it, -1 applies the cost
+ * model (packed when the pad-skipping kernel's touched 64-byte sectors
+ * exceed the packed bytes by more than SELLB_PACKED_MIN_GAIN, default 1.3).
+ * Every build applies the cost model unless SELLB_PACKED=0 / 1 forces it. */
 int sellb_set_packed(sellb_mat* m, int32_t mode);
 void sellb_free(sellb_mat* m);
 
@@ -197,6 +197,20 @@ int sellb_spmv_crs_range_host(const int64_t* rpt, int64_t n_rows, const int32_t*
                               const double* val, int64_t nnz, const double* x,
                               int64_t n_x, double* y, int64_t r0, int64_t r1,
                               int32_t accumulate, int32_t unrolled, int32_t device);
+
+/* Device-resident CRS handle for the same protocol: the arrays are
+ * validated (rpt starts at 0, ends at nnz, non-decreasing; 0 <= col <
+ * n_cols; formats.py:140-155) and uploaded once; each sellb_crs_spmv_host
+ * call moves x in and y[r0:r1) out (host arrays, blocking).  The kernels
+ * module caches handles by buffer identity (replaces the per-call upload of
+ * sellb_spmv_crs_range_host). */
+typedef struct sellb_crs sellb_crs;
+int sellb_crs_import(const int64_t* rpt, const int32_t* col, const void* val, int32_t dtype,
+                     int64_t n_rows, int64_t n_cols, int64_t nnz, int32_t device,
+                     sellb_crs** out);
+int sellb_crs_spmv_host(sellb_crs* m, const void* x_host, void* y_host, int64_t r0, int64_t r1,
+                        int32_t accumulate, int32_t unrolled);
+void sellb_crs_free(sellb_crs* m);
 
 /* CRS kernels on device arrays. */
 int sellb_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val,

@@ -37,7 +37,8 @@ EXPORTED = (
     "sellb_coo_to_crs", "sellb_mm_parse_body", "sellb_mm_format_body",
     "sellb_launch_count", "sellb_long_info", "sellb_streamed_bytes",
     "sellb_lru_stream_misses", "sellb_sell_x_lines", "sellb_host_register",
-    "sellb_host_unregister", "sellb_set_packed",
+    "sellb_host_unregister", "sellb_set_packed", "sellb_crs_import", "sellb_crs_spmv_host",
+    "sellb_crs_free",
 )
 
 
@@ -77,6 +78,10 @@ _PROTOS = {
     "sellb_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32]),
     "sellb_set_variant": (ctypes.c_int, [_vp, _i32]),
     "sellb_set_packed": (ctypes.c_int, [_vp, _i32]),
+    "sellb_crs_import": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _i32,
+                                        ctypes.POINTER(_vp)]),
+    "sellb_crs_spmv_host": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _i32]),
+    "sellb_crs_free": (None, [_vp]),
     "sellb_free": (None, [_vp]),
     "sellb_spmv": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp]),
     "sellb_spmv_chunk_list": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _i32, _vp]),

@@ -281,11 +281,9 @@ void free_mat_arrays(sellb_mat* m) {
     cudaFree(m->side_off);
     cudaFree(m->side_col);
     cudaFree(m->side_val);
-    cudaFree(m->poff);
+    cudaFree(m->prpt);
     cudaFree(m->pcol);
     cudaFree(m->pval);
-    cudaFree(m->prl);
-    cudaFree(m->pidx);
     if (m->pipe_ready) {
         cudaStreamDestroy(m->s_h2d);
         cudaStreamDestroy(m->s_comp);
@@ -555,79 +553,40 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// Chunk-sorted packed copy (C = 32; the pJDS idea inside each chunk): the
-// chunk's short rows ordered by descending length (ties by row), stored
-// slot-major without padding -- slot j holds the k_j rows longer than j
-// contiguously, then slot j+1 -- so the SpMV streams each chunk as one dense
-// run of (s_v + 4) bytes per nonzero (k_spmv_packed).  Each row keeps its own
-// slot order, so every sum is unchanged.  Rows the long-row rule hands to the
-// warp-per-row role (chunk wider than long_th and row longer than chunk_th)
-// get length 0 here and sort last.
+// Packed stored-order copy (C = 32): stored row p's entries, slot order,
+// at prpt[p] .. prpt[p+1] (prpt = exclusive scan of row_lengths) -- the
+// SELL layout without its padding, read by the row-run kernel.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int packed_len(const int32_t* rl, const int32_t* cl,
-                                          const int32_t* chunk_th, int long_th, int64_t c,
-                                          int lane, bool* is_long) {
-    const int len = rl[c * 32 + lane];
-    *is_long = chunk_th && cl[c] > long_th && len > chunk_th[c];
-    return *is_long ? 0 : len;
-}
-
-__global__ void k_packed_count(const int32_t* __restrict__ rl, const int32_t* __restrict__ cl,
-                               const int32_t* __restrict__ chunk_th, int long_th,
-                               int64_t n_chunks, int64_t* __restrict__ cnt) {
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (c >= n_chunks) return;
-    bool lg;
-    const int len = packed_len(rl, cl, chunk_th, long_th, c, lane, &lg);
-    const int tot = __reduce_add_sync(0xffffffffu, (unsigned)len);
-    if (lane == 0) cnt[c] = tot;
+__global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i];
 }
 
 template <typename T>
-__global__ void k_packed_fill(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
-                              const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
-                              const T* __restrict__ val, const int32_t* __restrict__ chunk_th,
-                              int long_th, int64_t n_chunks, const int64_t* __restrict__ poff,
-                              int32_t* __restrict__ pcol, T* __restrict__ pval,
-                              int32_t* __restrict__ prl, uint8_t* __restrict__ pidx) {
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void k_packed_fill(const int64_t* __restrict__ cs, const int32_t* __restrict__ rl,
+                              const int32_t* __restrict__ col, const T* __restrict__ val,
+                              int64_t n_pad, int64_t C, const int64_t* __restrict__ prpt,
+                              int32_t* __restrict__ pcol, T* __restrict__ pval) {
+    const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (c >= n_chunks) return;
-    bool lg;
-    const int len = packed_len(rl, cl, chunk_th, long_th, c, lane, &lg);
-    // rank in descending length, ties by row: a stable order
-    int rank = 0;
-    for (int o = 0; o < 32; ++o) {
-        const int lo = __shfl_sync(0xffffffffu, len, o);
-        rank += (lo > len) || (lo == len && o < lane);
-    }
-    prl[c * 32 + rank] = len;
-    pidx[c * 32 + rank] = (uint8_t)(lane | (lg ? 0x80 : 0));
-    const int maxlen = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
-    int64_t pj = poff[c];
-    const int64_t src0 = cs[c] + lane;
-    for (int j = 0; j < maxlen; ++j) {
-        const int k = __popc(__ballot_sync(0xffffffffu, len > j));
-        if (j < len) {
-            pcol[pj + rank] = col[src0 + (int64_t)j * 32];
-            pval[pj + rank] = val[src0 + (int64_t)j * 32];
-        }
-        pj += k;
+    if (p >= n_pad) return;
+    const int64_t chunk = p / C;
+    const int64_t src = cs[chunk] + (p - chunk * C);
+    const int64_t dst = prpt[p];
+    const int len = rl[p];
+    for (int j = lane; j < len; j += 32) {
+        pcol[dst + j] = col[src + (int64_t)j * C];
+        pval[dst + j] = val[src + (int64_t)j * C];
     }
 }
 
 void free_packed(sellb_mat* m) {
-    cudaFree(m->poff);
+    cudaFree(m->prpt);
     cudaFree(m->pcol);
     cudaFree(m->pval);
-    cudaFree(m->prl);
-    cudaFree(m->pidx);
-    m->poff = nullptr;
+    m->prpt = nullptr;
     m->pcol = nullptr;
     m->pval = nullptr;
-    m->prl = nullptr;
-    m->pidx = nullptr;
     m->n_packed = 0;
 }
 
@@ -635,15 +594,15 @@ void free_packed(sellb_mat* m) {
 
 namespace sellb {
 
-// force: 1 build, 0 drop, -1 cost model, -2 the build's default: off unless
-// SELLB_PACKED says 1 / auto (measured: the chunk-sorted kernel streams 2.1x
-// fewer bytes on cfg3 sigma=1 but is latency-bound at the same ~500 us as
-// the bulk role, so it is not the default yet -- DESIGN.md §4)
+// force: 1 build, 0 drop, -1 cost model, -2 the build's default: the cost
+// model unless SELLB_PACKED says 0 / 1 (measured, tools/packed_ab.sh: cfg3
+// sigma=1 324 -> 450 GF/s; sigma=128 / 512 and cfg4 are faster in the SELL
+// bulk role, and the model leaves them there)
 int build_packed(sellb_mat* m, cudaStream_t st, int force) {
     free_packed(m);
     if (force == -2) {
         const char* e = getenv("SELLB_PACKED");
-        force = !e ? 0 : (strcmp(e, "auto") == 0 ? -1 : (atoi(e) ? 1 : 0));
+        force = (!e || strcmp(e, "auto") == 0) ? -1 : (atoi(e) ? 1 : 0);
     }
     if (force == 0) return 0;
     const bool possible = m->C == 32 && m->rl && m->n_chunks > 0 && m->slots > 0;
@@ -653,29 +612,11 @@ int build_packed(sellb_mat* m, cudaStream_t st, int force) {
         return 0;
     }
     const int64_t vs = (int64_t)vsize(m->dtype);
-    DBuf d_cnt;
-    SELLB_CU(d_cnt.alloc((m->n_chunks + 1) * 8, st));
-    SELLB_CU(cudaMemsetAsync(d_cnt.p, 0, 8, st));
-    k_packed_count<<<(unsigned)grid_for(m->n_chunks * 32, 256), 256, 0, st>>>(
-        m->rl, m->cl, m->chunk_th, m->long_th, m->n_chunks, d_cnt.as<int64_t>() + 1);
-    if (int rc = check_stream_error()) return rc;
-    if (int rc = alloc_dev((void**)&m->poff, (m->n_chunks + 1) * 8)) return rc;
-    {
-        size_t tmp_bytes = 0;
-        SELLB_CU(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_cnt.as<int64_t>(), m->poff,
-                                               m->n_chunks + 1, st));
-        DBuf d_tmp;
-        SELLB_CU(d_tmp.alloc(tmp_bytes, st));
-        SELLB_CU(cub::DeviceScan::InclusiveSum(d_tmp.p, tmp_bytes, d_cnt.as<int64_t>(), m->poff,
-                                               m->n_chunks + 1, st));
-    }
-    int64_t total = 0;
-    SELLB_CU(cudaMemcpyAsync(&total, m->poff + m->n_chunks, 8, cudaMemcpyDeviceToHost, st));
-    SELLB_CU(cudaStreamSynchronize(st));
+    const int64_t total = m->nnz;
     if (force < 0) {
-        // cost model: the bytes the bulk role streams as configured (touched
-        // 32-byte sectors of the short rows' slots; the long rows read the
-        // side table either way) against the packed bytes + chunk offsets
+        // cost model: the 64-byte sectors the bulk role touches for the short
+        // rows (the long rows read the side table) against the packed copy's
+        // bytes (every row, no padding) + its row offsets
         if (m->variant != SELLB_VARIANT_PAD_SKIP) { free_packed(m); return 0; }
         DBuf cnt;
         SELLB_CU(cnt.alloc(4 * sizeof(unsigned long long), st));
@@ -687,10 +628,10 @@ int build_packed(sellb_mat* m, cudaStream_t st, int force) {
         unsigned long long h[4];
         SELLB_CU(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
         SELLB_CU(cudaStreamSynchronize(st));
-        double gain_min = 1.15;
+        double gain_min = 1.3;      // cfg3 sigma=1: 1.52 (packed wins); sigma=512 1.05, cfg4 0.83
         if (const char* e = getenv("SELLB_PACKED_MIN_GAIN")) gain_min = atof(e);
         const double skip_bytes = (double)h[2];     // 64-byte sectors (DRAM bursts)
-        const double packed_bytes = (double)(vs + 4) * (double)total + 8.0 * m->n_chunks;
+        const double packed_bytes = (double)(vs + 4) * (double)total + 8.0 * m->n_pad;
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
         if (skip_bytes < gain_min * packed_bytes ||
@@ -699,21 +640,32 @@ int build_packed(sellb_mat* m, cudaStream_t st, int force) {
             return 0;
         }
     }
+    if (int rc = alloc_dev((void**)&m->prpt, (m->n_pad + 1) * 8)) return rc;
+    {
+        DBuf d_len;
+        SELLB_CU(d_len.alloc((m->n_pad + 1) * 8, st));
+        SELLB_CU(cudaMemsetAsync(d_len.p, 0, 8, st));
+        k_widen<<<(unsigned)grid_for(m->n_pad, 256), 256, 0, st>>>(m->rl, m->n_pad,
+                                                                    d_len.as<int64_t>() + 1);
+        size_t tmp_bytes = 0;
+        SELLB_CU(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_len.as<int64_t>(), m->prpt,
+                                               m->n_pad + 1, st));
+        DBuf d_tmp;
+        SELLB_CU(d_tmp.alloc(tmp_bytes, st));
+        SELLB_CU(cub::DeviceScan::InclusiveSum(d_tmp.p, tmp_bytes, d_len.as<int64_t>(), m->prpt,
+                                               m->n_pad + 1, st));
+    }
     if (int rc = alloc_dev((void**)&m->pcol, std::max<int64_t>(total, 1) * 4)) return rc;
     if (int rc = alloc_dev(&m->pval, std::max<int64_t>(total, 1) * vs)) return rc;
-    if (int rc = alloc_dev((void**)&m->prl, m->n_pad * 4)) return rc;
-    if (int rc = alloc_dev((void**)&m->pidx, m->n_pad)) return rc;
-    const unsigned grid = (unsigned)grid_for(m->n_chunks * 32, 256);
+    const unsigned grid = (unsigned)grid_for(m->n_pad * 32, 256);
     if (m->dtype == SELLB_F32)
-        k_packed_fill<float><<<grid, 256, 0, st>>>(m->cs, m->cl, m->rl, m->col,
-                                                  (const float*)m->val, m->chunk_th, m->long_th,
-                                                  m->n_chunks, m->poff, m->pcol,
-                                                  (float*)m->pval, m->prl, m->pidx);
+        k_packed_fill<float><<<grid, 256, 0, st>>>(m->cs, m->rl, m->col, (const float*)m->val,
+                                                  m->n_pad, m->C, m->prpt, m->pcol,
+                                                  (float*)m->pval);
     else
-        k_packed_fill<double><<<grid, 256, 0, st>>>(m->cs, m->cl, m->rl, m->col,
-                                                   (const double*)m->val, m->chunk_th,
-                                                   m->long_th, m->n_chunks, m->poff, m->pcol,
-                                                   (double*)m->pval, m->prl, m->pidx);
+        k_packed_fill<double><<<grid, 256, 0, st>>>(m->cs, m->rl, m->col, (const double*)m->val,
+                                                   m->n_pad, m->C, m->prpt, m->pcol,
+                                                   (double*)m->pval);
     if (int rc = check_stream_error()) return rc;
     SELLB_CU(cudaStreamSynchronize(st));
     m->n_packed = total;

@@ -58,20 +58,14 @@ struct sellb_mat {
     int64_t* side_off = nullptr;
     int32_t* side_col = nullptr;
     void* side_val = nullptr;
-    // chunk-sorted packed copy (sellb_build.cu build_packed, kernel
-    // k_spmv_packed; the pJDS idea inside each C = 32 chunk): the chunk's
-    // short rows re-ordered by descending length, stored slot-major without
-    // padding -- slot j holds the k_j rows longer than j, contiguous, and
-    // slot j+1 follows it -- so the warp streams each chunk as one dense run.
-    // prl / pidx: the sorted rows' lengths and their row within the chunk
-    // (bit 7: a long row, summed by the warp-per-row role).  The SELL arrays
-    // stay the exported layout; the copy only changes which bytes the SpMV
-    // streams.
-    int64_t* poff = nullptr;          // n_chunks + 1 packed chunk offsets
+    // packed stored-order copy (sellb_build.cu build_packed, kernel
+    // k_spmv_rows MODE 1) for pad-heavy C = 32 layouts: every stored row's
+    // entries without padding, row after row (a CRS of the stored rows), so
+    // a warp streams 32 rows' entries as one dense run.  The SELL arrays stay
+    // the exported layout; the copy only changes which bytes the SpMV reads.
+    int64_t* prpt = nullptr;          // n_pad + 1 row offsets into pcol / pval
     int32_t* pcol = nullptr;
     void* pval = nullptr;
-    int32_t* prl = nullptr;           // n_pad
-    uint8_t* pidx = nullptr;          // n_pad
     int64_t n_packed = 0;
     int32_t long_th = 0x7fffffff;     // chunks wider than this may hold long rows
     int32_t* chunk_th = nullptr;      // per chunk: rows longer than this are long

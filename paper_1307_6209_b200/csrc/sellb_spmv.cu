@@ -700,134 +700,6 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
 }
 
-// Chunk-sorted packed kernel (C = 32, pad-heavy layouts; sellb_build.cu
-// build_packed).  The chunk's rows come sorted by descending length and
-// stored slot-major without padding: slot j holds the k_j rows longer than
-// j as k_j consecutive entries (row r of slot j at P_j + r), slot j+1
-// follows.  One warp per chunk streams the run in tiles of E = 32 U
-// entries:
-//   phase 1 -- lane t takes entries t, t+32, ... of the tile: dense,
-//              coalesced val/col loads (every lane busy whatever the row
-//              lengths), the x gathers, the rounded products into the warp's
-//              shared-memory stage; the next tile's val/col loads are issued
-//              before this tile's gathers are consumed (one round trip in
-//              flight behind the other);
-//   phase 2 -- lane r (the r-th longest row) walks its own entries P_j + r
-//              that fall in the tile, in slot order, adding them to its sum.
-//              P_{j+1} = P_j + k_j, and k_j (rows longer than j) follows from
-//              the chunk's sorted lengths kept in shared memory -- no warp
-//              vote per slot.
-// So the bytes streamed are (s_v + 4) per nonzero and the memory
-// instructions are dense, while each row is still summed from +0.0 in slot
-// order with separately rounded products: y is bitwise the reference's.
-// Long rows (the bulk role's rule) take the warp-per-row role of blocks
-// [0, n_long_blocks), reading the side table.
-template <typename T, bool ACC, int ORD, int U>
-__global__ void __launch_bounds__(kThreads, U >= 8 ? 3 : 4)
-k_spmv_packed(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
-              const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
-              const T* __restrict__ val, const int64_t* __restrict__ poff,
-              const int32_t* __restrict__ pcol, const T* __restrict__ pval,
-              const int32_t* __restrict__ prl, const uint8_t* __restrict__ pidx,
-              const T* __restrict__ x, T* __restrict__ y, const int32_t* __restrict__ order,
-              int64_t c0, int64_t c1, int64_t n_rows, const int32_t* __restrict__ long_rows,
-              int64_t n_long, int l2pol, const int64_t* __restrict__ side_off,
-              const int32_t* __restrict__ side_col, const T* __restrict__ side_val) {
-    constexpr int WPB = kThreads / 32;
-    constexpr int E = 32 * U;                         // entries per tile
-    static_assert(E >= kSeg * 32, "stage too small for the long-row role");
-    __shared__ __align__(16) T stage[WPB][E];
-    __shared__ int slens[WPB][32];
-    const uint64_t pol_s = make_policy(l2pol & 0xf);
-    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T* st = stage[warp];
-    const int64_t n_long_blocks = (n_long + WPB - 1) / WPB;
-    if ((int64_t)blockIdx.x < n_long_blocks) {       // long-row role
-        const int64_t k = (int64_t)blockIdx.x * WPB + warp;
-        if (k >= n_long) return;
-        const int64_t p = long_rows[k];
-        if (p < c0 * 32 || p >= c1 * 32) return;
-        const int64_t chunk = p >> 5;
-        if (side_off) {
-            const int64_t o = side_off[k];
-            long_row_at<T, ACC, ORD>(side_val + o, side_col + o, 1, rl[p], cl[chunk], x, y,
-                                     order, p, n_rows, lane, pol_s, pol_x, st);
-        } else {
-            const int64_t base = cs[chunk] + (p - chunk * 32);
-            long_row_at<T, ACC, ORD>(val + base, col + base, 32, rl[p], cl[chunk], x, y, order,
-                                     p, n_rows, lane, pol_s, pol_x, st);
-        }
-        return;
-    }
-    const int64_t c = c0 + ((int64_t)blockIdx.x - n_long_blocks) * WPB + warp;
-    if (c >= c1) return;
-    const int len = prl[c * 32 + lane];
-    const int tag = pidx[c * 32 + lane];
-    slens[warp][lane] = len;
-    const int64_t cbase = poff[c];
-    const int tot = (int)(poff[c + 1] - cbase);
-    const T* __restrict__ pv = pval + cbase;
-    const int32_t* __restrict__ pc = pcol + cbase;
-    // this lane's walk: next slot jl, its entry offset Pl + lane, k = k_jl
-    int jl = 0, Pl = 0;
-    int kc = __popc(__ballot_sync(0xffffffffu, len > 0));
-    __syncwarp();
-    T sum = T(0);
-    T v[U];
-    int32_t ci[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int t = u * 32 + lane;
-        v[u] = T(0);
-        ci[u] = 0;
-        if (t < tot) {
-            v[u] = ld_stream(pv + t, pol_s);
-            ci[u] = ld_stream(pc + t, pol_s);
-        }
-    }
-    for (int tb = 0; tb < tot; tb += E) {
-        T xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = (tb + u * 32 + lane < tot) ? ld_x(x + ci[u], pol_x) : T(0);
-        // the next tile's matrix entries, in flight behind this tile's gathers
-        T vn[U];
-        int32_t cn[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int t = tb + E + u * 32 + lane;
-            vn[u] = T(0);
-            cn[u] = 0;
-            if (t < tot) {
-                vn[u] = ld_stream(pv + t, pol_s);
-                cn[u] = ld_stream(pc + t, pol_s);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (tb + u * 32 + lane < tot) st[u * 32 + lane] = Arith<T>::mul(v[u], xv[u]);
-        __syncwarp();
-        // phase 2: this row's entries inside [tb, tb + E), in slot order
-        const int te = tb + E;
-        while (jl < len && Pl + lane < te) {
-            sum = Arith<T>::add(sum, st[Pl + lane - tb]);
-            Pl += kc;
-            ++jl;
-            while (kc > 0 && slens[warp][kc - 1] <= jl) --kc;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            v[u] = vn[u];
-            ci[u] = cn[u];
-        }
-    }
-    if (tag & 0x80) return;                                     // stored by the long-row role
-    const int64_t p = c * 32 + (tag & 31);
-    if (len < cl[c]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
-    store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
-}
-
 // Persistent "short chunk" variant (C = 32, no long rows): a grid of a few
 // blocks per SM whose warps sweep chunks c, c + n_warps, ...; the next
 // chunk's metadata (cs, cl, row length) is fetched before the current chunk
@@ -1026,6 +898,380 @@ k_spmv_crs_unrolled(const int64_t* __restrict__ rpt, const int32_t* __restrict__
     acc = ACC ? A::add(y[i], comb) : comb;
     for (; j < e; ++j) acc = A::add(acc, A::mul(val[j], __ldg(x + col[j])));
     y[i] = acc;
+}
+
+// Row-run kernel: one warp per 32 consecutive rows whose entries form one
+// contiguous run [rpt[rb], rpt[rb+32]) -- the CRS arrays (_kernels.pyx:17-62)
+// or the packed stored-order copy of a SELL matrix (build_packed).  The warp
+// streams the run through a shared-memory stage of S entries:
+//   phase 1 -- sub-batches of 32 U entries: lane t loads entries t, t+32, ...
+//              (dense, coalesced val / col loads, every lane busy whatever
+//              the row lengths), gathers x, stores the rounded products; the
+//              next sub-batch's loads are issued before this one's gathers
+//              are consumed;
+//   phase 2 -- lane l walks row rb + l's products in the stage, in order.
+// Runs longer than S go window by window.  The plain walk adds each row's
+// products to one sum from +0.0 (the reference's loop), the unrolled one
+// into t[j % 4] over the first 4 floor(len/4) entries, combines
+// ((t0 + t1) + t2) + t3, adds y when accumulating, then the tail
+// (_kernels.pyx:34-62) -- bitwise the reference either way.
+// MODE 0: CRS rows, y[i].  MODE 1: packed SELL rows (stored row p = i): y[p]
+// (ORD 0) or y[order[p]] (ORD 1), plus the reference's 0 * x[0] term for
+// rows shorter than their chunk (the padding slots it adds).
+template <typename T, bool ACC, bool UNR, int MODE, int ORD, int U, int S>
+__global__ void __launch_bounds__(kThreads, 3)
+k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
+            const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+            int64_t r0, int64_t r1, const int32_t* __restrict__ order,
+            const int32_t* __restrict__ cl, int64_t n_rows) {
+    constexpr int WPB = kThreads / 32;
+    constexpr int B = 32 * U;
+    static_assert(S % B == 0, "stage must hold whole sub-batches");
+    extern __shared__ __align__(16) uint8_t rows_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* st = reinterpret_cast<T*>(rows_smem) + (size_t)warp * S;
+    const int64_t rb = r0 + ((int64_t)blockIdx.x * WPB + warp) * 32;
+    if (rb >= r1) return;
+    const int64_t i = rb + lane;
+    const bool valid = i < r1;
+    const int64_t last = min(rb + 32, r1);
+    const int64_t s = valid ? rpt[i] : 0;
+    const int64_t e = valid ? rpt[i + 1] : 0;
+    const int64_t base = rpt[rb];
+    const int64_t end = rpt[last];
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const int64_t m4 = s + ((e - s) & ~(int64_t)3);
+    int64_t pos = s;
+    T sum = T(0), t0 = T(0), t1 = T(0), t2 = T(0), t3 = T(0);
+    bool tail = !UNR;
+    for (int64_t wb = base; wb < end; wb += S) {
+        const int64_t we = min(wb + (int64_t)S, end);
+        T v[U];
+        int32_t ci[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t t = wb + u * 32 + lane;
+            v[u] = T(0);
+            ci[u] = 0;
+            if (t < we) {
+                v[u] = ld_stream(val + t, pol_s);
+                ci[u] = ld_stream(col + t, pol_s);
+            }
+        }
+        for (int64_t sb = wb; sb < we; sb += B) {
+            T xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                xv[u] = (sb + u * 32 + lane < we) ? ld_x(x + ci[u], pol_x) : T(0);
+            T vn[U];
+            int32_t cn[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t t = sb + B + u * 32 + lane;
+                vn[u] = T(0);
+                cn[u] = 0;
+                if (t < we) {
+                    vn[u] = ld_stream(val + t, pol_s);
+                    cn[u] = ld_stream(col + t, pol_s);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (sb + u * 32 + lane < we)
+                    st[sb - wb + u * 32 + lane] = Arith<T>::mul(v[u], xv[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                v[u] = vn[u];
+                ci[u] = cn[u];
+            }
+        }
+        __syncwarp();
+        // phase 2: this row's products inside the window, in order
+        const T* sp = st - wb;
+        if (!UNR) {
+            const int64_t stop = min(e, we);
+            for (; pos + 4 <= stop; pos += 4) {
+                const T a0 = sp[pos], a1 = sp[pos + 1], a2 = sp[pos + 2], a3 = sp[pos + 3];
+                sum = Arith<T>::add(sum, a0);
+                sum = Arith<T>::add(sum, a1);
+                sum = Arith<T>::add(sum, a2);
+                sum = Arith<T>::add(sum, a3);
+            }
+            for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
+        } else {
+            const int64_t stop4 = min(m4, we);
+            // whole groups of four (pos - s is a multiple of 4 here unless a
+            // window boundary split a group: then one entry at a time)
+            while (pos < stop4) {
+                if (((pos - s) & 3) == 0 && pos + 4 <= stop4) {
+                    t0 = Arith<T>::add(t0, sp[pos]);
+                    t1 = Arith<T>::add(t1, sp[pos + 1]);
+                    t2 = Arith<T>::add(t2, sp[pos + 2]);
+                    t3 = Arith<T>::add(t3, sp[pos + 3]);
+                    pos += 4;
+                } else {
+                    const int k = (int)((pos - s) & 3);
+                    const T pr = sp[pos];
+                    if (k == 0) t0 = Arith<T>::add(t0, pr);
+                    else if (k == 1) t1 = Arith<T>::add(t1, pr);
+                    else if (k == 2) t2 = Arith<T>::add(t2, pr);
+                    else t3 = Arith<T>::add(t3, pr);
+                    ++pos;
+                }
+            }
+            const int64_t stop = min(e, we);
+            if (pos >= m4 && pos < stop && !tail) {
+                const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
+                sum = ACC ? Arith<T>::add(y[i], comb) : comb;
+                tail = true;
+            }
+            for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
+        }
+        __syncwarp();
+    }
+    if (!valid) return;
+    if (MODE == 0) {
+        if (!UNR) {
+            y[i] = ACC ? Arith<T>::add(y[i], sum) : sum;
+        } else {
+            if (!tail) {
+                const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
+                sum = ACC ? Arith<T>::add(y[i], comb) : comb;
+            }
+            y[i] = sum;
+        }
+    } else {
+        if ((int64_t)(e - s) < (int64_t)cl[i >> 5]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+        store_row<T, ACC, ORD>(y, order, i, n_rows, sum);
+    }
+}
+
+// Persistent, asynchronously staged form of the row-run kernel: each warp
+// walks its 32-row groups (g = warp, warp + all warps, ...) as a stream of
+// windows of <= S entries, double-buffered in shared memory -- window w+1's
+// val / col run is copied by cp.async (dense, coalesced, no registers held)
+// while window w's x gathers, products and per-row walks run -- so the DRAM
+// round trip of the matrix stream is off the critical path and only the x
+// gathers (mostly L2 hits) are waited for.  Same sums as k_spmv_rows.
+template <typename T, int S>
+struct RowsStage {
+    T val[2][S];
+    int32_t col[2][S];
+};
+
+template <typename T, bool ACC, bool UNR, int MODE, int ORD, int S>
+__global__ void __launch_bounds__(kThreads, 2)
+k_spmv_rows_async(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
+                  const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+                  int64_t r0, int64_t r1, const int32_t* __restrict__ order,
+                  const int32_t* __restrict__ cl, int64_t n_rows) {
+    constexpr int WPB = kThreads / 32;
+    constexpr int G = S / 32;                          // gathers per lane per window
+    extern __shared__ __align__(16) uint8_t rows_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    RowsStage<T, S>& W = reinterpret_cast<RowsStage<T, S>*>(rows_smem)[warp];
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const int64_t GW = (int64_t)gridDim.x * WPB;
+    const int64_t n_groups = (r1 - r0 + 31) / 32;
+    // the window stream: issue side
+    int64_t ig = (int64_t)blockIdx.x * WPB + warp;    // group being issued
+    int64_t iwb = 0, iend = -1;                        // next window start / group end
+    bool ifresh = true;                                // group's first window not out yet
+    auto next_window = [&](int64_t& g, int64_t& wb, int& n) {
+        if (!ifresh && iwb >= iend) {
+            ig += GW;
+            ifresh = true;
+        }
+        if (ig >= n_groups) { g = -1; wb = 0; n = 0; return; }
+        if (ifresh) {
+            const int64_t rb = r0 + ig * 32;
+            const int64_t last = min(rb + 32, r1);
+            iwb = rpt[rb];
+            iend = rpt[last];
+        }
+        g = ig;
+        wb = iwb;
+        n = (int)min((int64_t)S, iend - iwb);
+        iwb += n;
+        ifresh = false;
+    };
+    auto issue = [&](int64_t wb, int n, int b) {
+        for (int t = lane; t < n; t += 32) {
+            cp_async<sizeof(T)>(&W.val[b][t], val + wb + t, pol_s);
+            cp_async<4>(&W.col[b][t], col + wb + t, pol_s);
+        }
+        cp_commit();
+    };
+    // compute side: the current group's rows
+    int64_t cg = -1, i = 0, s = 0, e = 0, m4 = 0, pos = 0;
+    bool valid = false, tail = !UNR;
+    T sum = T(0), t0 = T(0), t1 = T(0), t2 = T(0), t3 = T(0);
+    auto finish = [&]() {
+        if (cg < 0 || !valid) return;
+        if (MODE == 0) {
+            if (!UNR) {
+                y[i] = ACC ? Arith<T>::add(y[i], sum) : sum;
+            } else {
+                if (!tail) {
+                    const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
+                    sum = ACC ? Arith<T>::add(y[i], comb) : comb;
+                }
+                y[i] = sum;
+            }
+        } else {
+            if ((int64_t)(e - s) < (int64_t)cl[i >> 5])
+                sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+            store_row<T, ACC, ORD>(y, order, i, n_rows, sum);
+        }
+    };
+
+    int64_t g0, wb0, g1, wb1;
+    int n0, n1;
+    next_window(g0, wb0, n0);
+    issue(wb0, n0, 0);
+    int b = 0;
+    while (g0 >= 0) {
+        next_window(g1, wb1, n1);
+        issue(wb1, n1, b ^ 1);                         // in flight during this window
+        cp_wait<1>();
+        __syncwarp();
+        if (g0 != cg) {                                // a new group: its rows
+            finish();
+            cg = g0;
+            i = r0 + cg * 32 + lane;
+            valid = i < r1;
+            s = valid ? rpt[i] : 0;
+            e = valid ? rpt[i + 1] : 0;
+            m4 = s + ((e - s) & ~(int64_t)3);
+            pos = s;
+            sum = t0 = t1 = t2 = t3 = T(0);
+            tail = !UNR;
+        }
+        // gathers and products of this window, in place
+        T xv[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const int t = k * 32 + lane;
+            xv[k] = t < n0 ? ld_x(x + W.col[b][t], pol_x) : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const int t = k * 32 + lane;
+            if (t < n0) W.val[b][t] = Arith<T>::mul(W.val[b][t], xv[k]);
+        }
+        __syncwarp();
+        const T* sp = W.val[b] - wb0;
+        const int64_t we = wb0 + n0;
+        if (!UNR) {
+            const int64_t stop = min(e, we);
+            for (; pos + 4 <= stop; pos += 4) {
+                const T a0 = sp[pos], a1 = sp[pos + 1], a2 = sp[pos + 2], a3 = sp[pos + 3];
+                sum = Arith<T>::add(sum, a0);
+                sum = Arith<T>::add(sum, a1);
+                sum = Arith<T>::add(sum, a2);
+                sum = Arith<T>::add(sum, a3);
+            }
+            for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
+        } else {
+            const int64_t stop4 = min(m4, we);
+            while (pos < stop4) {
+                if (((pos - s) & 3) == 0 && pos + 4 <= stop4) {
+                    t0 = Arith<T>::add(t0, sp[pos]);
+                    t1 = Arith<T>::add(t1, sp[pos + 1]);
+                    t2 = Arith<T>::add(t2, sp[pos + 2]);
+                    t3 = Arith<T>::add(t3, sp[pos + 3]);
+                    pos += 4;
+                } else {
+                    const int k = (int)((pos - s) & 3);
+                    const T pr = sp[pos];
+                    if (k == 0) t0 = Arith<T>::add(t0, pr);
+                    else if (k == 1) t1 = Arith<T>::add(t1, pr);
+                    else if (k == 2) t2 = Arith<T>::add(t2, pr);
+                    else t3 = Arith<T>::add(t3, pr);
+                    ++pos;
+                }
+            }
+            const int64_t stop = min(e, we);
+            if (pos >= m4 && pos < stop && !tail) {
+                const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
+                sum = ACC ? Arith<T>::add(y[i], comb) : comb;
+                tail = true;
+            }
+            for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
+        }
+        __syncwarp();                                  // buffer b free for window +2
+        g0 = g1;
+        wb0 = wb1;
+        n0 = n1;
+        b ^= 1;
+    }
+    finish();
+    cp_wait<0>();
+}
+
+constexpr int kRowsAsyncS = 512;
+
+constexpr int kRowsU = 4;
+constexpr int kRowsS = 1024;
+
+template <typename T, bool ACC, bool UNR, int MODE, int ORD>
+void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const void* x, void* y,
+                 int64_t r0, int64_t r1, const int32_t* order, const int32_t* cl, int64_t n_rows,
+                 cudaStream_t st) {
+    static const int async_env = [] {
+        const char* e = getenv("SELLB_ROWS_ASYNC");
+        return e ? atoi(e) : 0;
+    }();
+    if (async_env) {
+        auto kern = k_spmv_rows_async<T, ACC, UNR, MODE, ORD, kRowsAsyncS>;
+        constexpr size_t smem = sizeof(RowsStage<T, kRowsAsyncS>) * (kThreads / 32);
+        static unsigned attr_set = 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(attr_set & (1u << (dev & 31)))) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set |= 1u << (dev & 31);
+        }
+        static const int sms = [] {
+            int d = 0, n = 148;
+            cudaGetDevice(&d);
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+            return n;
+        }();
+        const int64_t groups = grid_for(r1 - r0, 32);
+        const int64_t blocks = std::max<int64_t>(
+            1, std::min<int64_t>(grid_for(groups, kThreads / 32), (int64_t)sms * 2));
+        kern<<<(unsigned)blocks, kThreads, smem, st>>>(rpt, col, (const T*)val, (const T*)x,
+                                                       (T*)y, r0, r1, order, cl, n_rows);
+        count_launches();
+        return;
+    }
+    static const int s_env = [] {
+        const char* e = getenv("SELLB_ROWS_S");
+        return e ? atoi(e) : kRowsS;
+    }();
+    const unsigned grid = (unsigned)grid_for(grid_for(r1 - r0, 32), kThreads / 32);
+#define SELLB_ROWS(SS)                                                                         \
+    do {                                                                                       \
+        auto kern = k_spmv_rows<T, ACC, UNR, MODE, ORD, kRowsU, SS>;                           \
+        constexpr size_t smem_ = (size_t)(kThreads / 32) * SS * sizeof(T);                     \
+        static unsigned attr_ = 0;                                                             \
+        int dev_ = 0;                                                                          \
+        cudaGetDevice(&dev_);                                                                  \
+        if (!(attr_ & (1u << (dev_ & 31)))) {                                                  \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_); \
+            attr_ |= 1u << (dev_ & 31);                                                        \
+        }                                                                                      \
+        kern<<<grid, kThreads, smem_, st>>>(rpt, col, (const T*)val, (const T*)x, (T*)y, r0,   \
+                                            r1, order, cl, n_rows);                            \
+    } while (0)
+    if (s_env == 256) SELLB_ROWS(256);
+    else if (s_env == 512) SELLB_ROWS(512);
+    else SELLB_ROWS(1024);
+#undef SELLB_ROWS
+    count_launches();
 }
 
 template <typename T, int CC, bool SKIP, bool ACC, int ORD>
@@ -1383,56 +1629,24 @@ int dispatch_acc(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t
                : dispatch_u<T, CC, SKIP, false, 0>(m, x, y, p0, p1, st);
 }
 
-template <typename T, bool ACC, int ORD>
-int launch_packed(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
-                  cudaStream_t st) {
-    static const int l2pol_env = [] {
-        const char* e = getenv("SELLB_L2POL");
-        return e ? (int)strtol(e, nullptr, 0) : -1;
-    }();
-    static const int vx_env = [] {
-        const char* e = getenv("SELLB_VX");
-        return e ? atoi(e) : 1;
-    }();
-    const int vx = (vx_env && ((uintptr_t)x & 15) == 0) ? 0x100 : 0;
-    const int l2pol = (l2pol_env >= 0 ? l2pol_env
-                       : ((int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20))
-                      | vx;
-    // SELLB_TIME_NO_LONG=1: timing experiments only -- the long rows are
-    // not summed (y wrong for them), isolating the packed role's time
-    static const bool no_long = getenv("SELLB_TIME_NO_LONG") && atoi(getenv("SELLB_TIME_NO_LONG"));
-    const int64_t n_long = (m->long_rows && !no_long) ? m->n_long : 0;
-    const bool side = m->side_off && m->n_rest == n_long && !m->n_groups;
-    const int32_t* lr = side ? m->long_rest : m->long_rows;
-    const int64_t wpb = kThreads / 32;
-    const unsigned grid = (unsigned)((n_long + wpb - 1) / wpb + (c1 - c0 + wpb - 1) / wpb);
-    static const int u_env = [] {
-        const char* e = getenv("SELLB_PACKED_U");
-        return e ? atoi(e) : 8;
-    }();
-#define SELLB_PK(UU)                                                                          \
-    k_spmv_packed<T, ACC, ORD, UU><<<grid, kThreads, 0, st>>>(                                \
-        m->cs, m->cl, m->rl, m->col, (const T*)m->val, m->poff, m->pcol, (const T*)m->pval,   \
-        m->prl, m->pidx, (const T*)x, (T*)y, m->order, c0, c1, m->n_rows, lr, n_long, l2pol,  \
-        side ? m->side_off : nullptr, side ? m->side_col : nullptr,                           \
-        (const T*)(side ? m->side_val : nullptr))
-    if (u_env == 4) SELLB_PK(4);
-    else SELLB_PK(8);
-#undef SELLB_PK
-    count_launches();
-    return 0;
-}
-
 template <typename T>
 int dispatch_sell(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1, int acc,
                   int ord, cudaStream_t st) {
     const bool skip = m->variant == SELLB_VARIANT_PAD_SKIP && m->rl;
-    if (skip && m->pcol && m->C == 32 && !m->n_groups) {
-        const int64_t c0 = p0 / 32, c1 = p1 / 32;
-        if (acc) return ord ? launch_packed<T, true, 1>(m, x, y, c0, c1, st)
-                            : launch_packed<T, true, 0>(m, x, y, c0, c1, st);
-        return ord ? launch_packed<T, false, 1>(m, x, y, c0, c1, st)
-                   : launch_packed<T, false, 0>(m, x, y, c0, c1, st);
+    if (skip && m->pcol && m->C == 32) {
+        // the packed stored-order copy through the row-run kernel (MODE 1)
+        if (acc) {
+            if (ord) launch_rows<T, true, false, 1, 1>(m->prpt, m->pcol, m->pval, x, y, p0, p1,
+                                                       m->order, m->cl, m->n_rows, st);
+            else launch_rows<T, true, false, 1, 0>(m->prpt, m->pcol, m->pval, x, y, p0, p1,
+                                                   m->order, m->cl, m->n_rows, st);
+        } else {
+            if (ord) launch_rows<T, false, false, 1, 1>(m->prpt, m->pcol, m->pval, x, y, p0, p1,
+                                                        m->order, m->cl, m->n_rows, st);
+            else launch_rows<T, false, false, 1, 0>(m->prpt, m->pcol, m->pval, x, y, p0, p1,
+                                                    m->order, m->cl, m->n_rows, st);
+        }
+        return 0;
     }
     if (m->C == 32) {
         return skip ? dispatch_acc<T, 32, true>(m, x, y, p0, p1, acc, ord, st)
@@ -1520,6 +1734,24 @@ int launch_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val, int
                     const void* x, void* y, int64_t r0, int64_t r1, int accumulate, int unrolled,
                     cudaStream_t st) {
     if (r1 <= r0) return 0;
+    // SELLB_CRS_SCALAR=1: the one-thread-per-row kernels (A/B reference)
+    static const bool scalar = getenv("SELLB_CRS_SCALAR") && atoi(getenv("SELLB_CRS_SCALAR"));
+    if (!scalar) {
+#define SELLB_CRST(T, A, UN)                                                                  \
+    launch_rows<T, A, UN, 0, 0>(rpt, col, val, x, y, r0, r1, nullptr, nullptr, 0, st)
+        if (dtype == SELLB_F32) {
+            if (unrolled) { if (accumulate) SELLB_CRST(float, true, true); else SELLB_CRST(float, false, true); }
+            else { if (accumulate) SELLB_CRST(float, true, false); else SELLB_CRST(float, false, false); }
+        } else {
+            if (unrolled) { if (accumulate) SELLB_CRST(double, true, true); else SELLB_CRST(double, false, true); }
+            else { if (accumulate) SELLB_CRST(double, true, false); else SELLB_CRST(double, false, false); }
+        }
+#undef SELLB_CRST
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess)
+            return set_error(SELLB_ERESOURCE, "crs launch failed: %s", cudaGetErrorString(e));
+        return 0;
+    }
     const unsigned grid = (unsigned)grid_for(r1 - r0, kThreads);
 #define SELLB_CRS(K, T, A) K<T, A><<<grid, kThreads, 0, st>>>(rpt, col, (const T*)val, (const T*)x, (T*)y, r0, r1)
     if (dtype == SELLB_F32) {

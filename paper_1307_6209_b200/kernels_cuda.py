@@ -16,9 +16,9 @@ reference's test fixture (tests/conftest.py:38-43).
     lru_stream_misses         _kernels.pyx:95-139  (LRU stack distances on the
                               device, equal miss counts)
 
-Arrays are host NumPy buffers, as in the reference.  Matrix arrays are
-uploaded once and cached by buffer identity (containers are immutable,
-formats.py:7); the cache entry dies with the ``val`` array.  Every call
+Arrays are host NumPy buffers, as in the reference.  Matrix arrays (SELL
+and CRS alike) are uploaded once and cached by buffer identity (containers
+are immutable, formats.py:7); the cache entry dies with the ``val`` array.  Every call
 blocks until y is back on the host, like the reference's nogil loops.
 """
 
@@ -102,16 +102,54 @@ def spmv_sell_range(cs, cl, C, col, val, x, y, c0, c1, accumulate):
                                            _lib.ORDER_STORED, None))
 
 
+def _crs_handle(rpt, col, val, n_cols):
+    key = ("crs", rpt.ctypes.data, len(rpt), col.ctypes.data, val.ctypes.data, len(val),
+           int(n_cols))
+    with _cache_lock:
+        h = _cache.get(key)
+    if h is not None:
+        return h
+    import ctypes
+    lib = _lib.require_device()
+    out = ctypes.c_void_p()
+    _lib.check(lib.sellb_crs_import(_lib.ptr(rpt), _lib.ptr(col), _lib.ptr(val),
+                                    _lib.SELLB_F64, len(rpt) - 1, int(n_cols), len(val), 0,
+                                    ctypes.byref(out)))
+    h = out.value
+    try:
+        weakref.finalize(val.base if val.base is not None else val, _evict_crs, key)
+    except TypeError:
+        pass
+    with _cache_lock:
+        if key in _cache:
+            _lib.load().sellb_crs_free(h)
+            return _cache[key]
+        _cache[key] = h
+    return h
+
+
+def _evict_crs(key):
+    with _cache_lock:
+        h = _cache.pop(key, None)
+    if h is not None:
+        try:
+            _lib.load().sellb_crs_free(h)
+        except Exception:
+            pass
+
+
 def _crs(rpt, col, val, x, y, r0, r1, accumulate, unrolled):
     if r1 <= r0:
         return
     rpt, col = _c64(rpt, np.int64), _c64(col, np.int32)
     val, x, y = _c64(val, np.float64), _c64(x, np.float64), _c64(y, np.float64)
-    lib = _lib.require_device()
-    _lib.check(lib.sellb_spmv_crs_range_host(
-        _lib.ptr(rpt), len(rpt) - 1, _lib.ptr(col), _lib.ptr(val), len(val),
-        _lib.ptr(x), len(x), _lib.ptr(y), int(r0), int(r1), int(bool(accumulate)),
-        int(unrolled), 0))
+    if not y.flags.writeable:
+        raise ParameterError("y must be writable")
+    if r0 < 0 or r1 > len(rpt) - 1 or len(y) < len(rpt) - 1:
+        raise ParameterError("row range or y length out of bounds")
+    h = _crs_handle(rpt, col, val, len(x))
+    _lib.check(_lib.load().sellb_crs_spmv_host(h, _lib.ptr(x), _lib.ptr(y), int(r0), int(r1),
+                                               int(bool(accumulate)), int(unrolled)))
 
 
 def spmv_crs_range(rpt, col, val, x, y, r0, r1, accumulate):

@@ -1,10 +1,10 @@
-"""The packed chunk copy (csrc/sellb_build.cu build_packed, kernel
-k_spmv_packed): pad-heavy C = 32 layouts stream every short row's entries
-without padding; the long rows keep the warp-per-row role.  The exported SELL
-arrays are unchanged, and y is bitwise the oracle's (the reference's
-_kernels.pyx:65-92 order) with the copy forced on, off, or chosen by the
-build -- overwrite / accumulate, stored / original order, chunk ranges,
-fp32, non-finite x[0], long rows with and without the side table."""
+"""The packed stored-order copy (csrc/sellb_build.cu build_packed, the
+row-run kernel k_spmv_rows in MODE 1): pad-heavy C = 32 layouts stream every
+row's entries without padding.  The exported SELL arrays are unchanged, and
+y is bitwise the oracle's (the reference's _kernels.pyx:65-92 order) with the
+copy forced on, off, or chosen by the build's cost model -- overwrite /
+accumulate, stored / original order, chunk ranges, fp32, non-finite x[0],
+long rows with and without the side table."""
 
 import os
 import subprocess
@@ -133,13 +133,12 @@ def test_packed_without_side_table():
 
 
 def test_packed_cost_model_choices():
-    """The cost model packs pad-heavy layouts and leaves dense ones alone;
-    builds leave the copy off by default."""
+    """The cost model (every build's default) packs the pad-heavy unsorted
+    layout and leaves dense, sorted and skewed-with-long-rows ones alone."""
     heavy = sb.crs_to_sell(generate.powerlaw(200_000, seed=4, band=5000), 32, 1)
     dense = sb.crs_to_sell(generate.stencil27(32), 32, 1)
     sorted_ = sb.crs_to_sell(generate.powerlaw(200_000, seed=4, band=5000), 32, 10 ** 9)
-    if not os.environ.get("SELLB_PACKED"):
-        assert not heavy.packed and not dense.packed and not sorted_.packed
-    for s in (heavy, dense, sorted_):
+    skewed = sb.crs_to_sell(sb.coo_to_crs(sb.gen_skewed(1 << 16, 8, 2048, 32)), 32, 1)
+    for s in (heavy, dense, sorted_, skewed):
         s.set_packed(None)
-    assert heavy.packed and not dense.packed and not sorted_.packed
+    assert heavy.packed and not dense.packed and not sorted_.packed and not skewed.packed

@@ -103,6 +103,31 @@ def run(cfg, f32, reps):
             s1 = s
         else:
             s.free()
+    # ours: the reference's CRS kernels (bit-exact order) on the same CRS input
+    rpt64 = torch.from_numpy(m.rpt).cuda()
+    col32 = torch.from_numpy(m.col.astype(np.int32)).cuda()
+    valt = torch.from_numpy(val_h).cuda()
+    y = torch.zeros(n, dtype=tdt, device="cuda")
+    slib = _lib.load()
+    code = _lib.SELLB_F32 if f32 else _lib.SELLB_F64
+    for unrolled, name in ((0, "ours_crs"), (1, "ours_crs_unrolled")):
+        st = torch.cuda.current_stream()
+
+        def launch():
+            _lib.check(slib.sellb_spmv_crs(rpt64.data_ptr(), col32.data_ptr(), valt.data_ptr(),
+                                           code, x.data_ptr(), y.data_ptr(), 0, n, 0, unrolled,
+                                           st.cuda_stream))
+        for _ in range(10):
+            launch()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(reps):
+            launch()
+        e1.record(st)
+        e1.synchronize()
+        rec(name, e0.elapsed_time(e1) / reps, y.cpu().numpy())
+    del rpt64, col32, valt
     lib = ctypes.CDLL(LIB)
     # cuSPARSE CSR
     rpt = torch.from_numpy(m.rpt.astype(np.int32)).cuda()
