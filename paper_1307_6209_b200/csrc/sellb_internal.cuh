@@ -75,11 +75,6 @@ struct sellb_mat {
     cudaStream_t s_long = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::mutex long_mu;
-    // TMA tensor maps of val / col viewed as 2-D [slots / C][C] (lazily
-    // encoded; the isolated-long-row kernel, sellb_tma_long.cu)
-    CUtensorMap tm_val{}, tm_col{};
-    int tm_state = 0;                 // 0 not tried, 1 ready, -1 not possible
-    std::mutex tm_mu;
     // end-to-end staging (device x / y for sellb_spmv_host)
     void* x_buf = nullptr;
     void* y_buf = nullptr;
@@ -157,12 +152,6 @@ int launch_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val, int
 int launch_spmv_tma(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
                     int accumulate, cudaStream_t st, const int64_t* h_cs);
 
-// sellb_tma_long.cu: warp per long row, val/col boxes by TMA; returns 1 if
-// launched, 0 if the layout does not qualify (C % 4, no tensor map)
-int launch_long_tma(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1,
-                    int accumulate, int out_order, const int32_t* rows, int64_t n_rows_list,
-                    int l2pol, cudaStream_t st);
-bool long_tma_possible(const sellb_mat* m);
 
 // sellb_host.cu: host staging of pageable vectors
 void host_parallel_copy(void* dst, const void* src, size_t n);

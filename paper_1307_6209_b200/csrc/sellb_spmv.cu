@@ -306,19 +306,8 @@ __device__ __forceinline__ void long_row_at(const T* __restrict__ vp,
 }
 
 // ---------------------------------------------------------------------------
-// Pipelined long-row kernel (its own launch, on a side stream next to the
-// bulk): still one warp per long row and the same staged, in-order add chain
-// as long_row(), but the loads are asynchronous copies into a per-warp
-// shared-memory ring, so the chain of batch b runs while the val/col of
-// batches b+1..b+D-1 and the x gather of batch b+1 are in flight.  The
-// warp-per-row role inside the bulk kernel has one batch in flight and is
-// latency-bound (cfg4 sigma=N: 1024 rows of 2048 took 64 us of a 66 us SpMV).
-//   group order per batch b:  VC(b+D) [val, col]  then  X(b+1) [x[col]]
-// cp.async with a 4 / 8-byte copy size (each lane its own slot), L1-allocating
-// (.ca): the 8 warps of a block walk 8 adjacent rows of the same chunk, so
-// one warp's sectors are the next warp's L1 hits.
+// cp.async ring helpers (the row-group kernel below)
 // ---------------------------------------------------------------------------
-constexpr int kLB = 128;                 // slots per batch (4 per lane)
 
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -347,107 +336,6 @@ template <int E>
 __device__ __forceinline__ void wait_x(int b) {
     if (b >= E - 1) cp_wait<2 * E>();
     else cp_wait<E + 1>();
-}
-
-template <typename T, bool ACC, int ORD, int D, int E>
-__global__ void __launch_bounds__(kThreads)
-k_spmv_long(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
-            const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
-            const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
-            const int32_t* __restrict__ order, int64_t C, int64_t p0, int64_t p1,
-            int64_t n_rows, const int32_t* __restrict__ long_rows, int64_t n_long, int l2pol) {
-    constexpr int NS = D + 1;                              // ring stages
-    extern __shared__ __align__(16) uint8_t lsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t k = (int64_t)blockIdx.x * (kThreads / 32) + warp;
-    if (k >= n_long) return;
-    const int64_t p = long_rows[k];
-    if (p < p0 || p >= p1) return;
-    // per-warp ring: NS x {val[kLB], x[kLB]} of T, NS x col[kLB] int32
-    T* sv = reinterpret_cast<T*>(lsm) + (size_t)warp * NS * 2 * kLB;
-    T* sx = sv + NS * kLB;
-    int32_t* sc = reinterpret_cast<int32_t*>(reinterpret_cast<T*>(lsm) +
-                                             (size_t)(kThreads / 32) * NS * 2 * kLB) +
-                  (size_t)warp * NS * kLB;
-    const uint64_t pol_s = make_policy(l2pol & 0xf);
-    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
-    const int64_t chunk = p / C;
-    const int64_t base = cs[chunk] + (p - chunk * C);
-    const int w = cl[chunk];
-    const int len = rl[p];
-    const int nb = (len + kLB - 1) / kLB;
-    const T* vp = val + base;
-    const int32_t* cp = col + base;
-
-    auto issue_vc = [&](int b) {
-        if (b < nb) {
-            const int st = b % NS;
-#pragma unroll
-            for (int s = 0; s < kLB / 32; ++s) {
-                const int j = b * kLB + s * 32 + lane;
-                if (j < len) {
-                    cp_async<sizeof(T)>(sv + st * kLB + s * 32 + lane, vp + (int64_t)j * C, pol_s);
-                    cp_async<4>(sc + st * kLB + s * 32 + lane, cp + (int64_t)j * C, pol_s);
-                }
-            }
-        }
-        cp_commit();
-    };
-    auto issue_x = [&](int b) {       // needs this lane's col of batch b landed
-        if (b < nb) {
-            const int st = b % NS;
-#pragma unroll
-            for (int s = 0; s < kLB / 32; ++s) {
-                const int j = b * kLB + s * 32 + lane;
-                if (j < len) cp_async<sizeof(T)>(sx + st * kLB + s * 32 + lane,
-                                                 x + sc[st * kLB + s * 32 + lane], pol_x);
-            }
-        }
-        cp_commit();
-    };
-
-#pragma unroll
-    for (int b = 0; b < D; ++b) issue_vc(b);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        cp_wait<D - 1>();                                  // VC(e)
-        issue_x(e);
-    }
-    T sum = T(0);
-    for (int b = 0; b < nb; ++b) {
-        issue_vc(b + D);
-        wait_vc<D, E>(b);                                  // VC(b+E)
-        issue_x(b + E);
-        wait_x<E>(b);                                      // X(b)
-        const int st = b % NS;
-#pragma unroll
-        for (int s = 0; s < kLB / 32; ++s) {               // rounded products, in place
-            const int i = st * kLB + s * 32 + lane;
-            const int j = b * kLB + s * 32 + lane;
-            sv[i] = (j < len) ? Arith<T>::mul(sv[i], sx[i]) : T(0);
-        }
-        __syncwarp();
-        const T* pr = sv + st * kLB;
-        const int cnt = min(len - b * kLB, kLB);
-        int i = 0;
-        for (; i + 16 <= cnt; i += 16) {
-            T q[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) q[u] = pr[i + u];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) sum = Arith<T>::add(sum, q[u]);
-        }
-        for (; i < cnt; ++i) sum = Arith<T>::add(sum, pr[i]);
-        __syncwarp();                                      // stage free for VC(b+NS)
-    }
-    cp_wait<0>();
-    if (len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
-    if (lane == 0) store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
-}
-
-template <typename T, int D>
-constexpr size_t long_smem() {
-    return (size_t)(kThreads / 32) * (D + 1) * kLB * (2 * sizeof(T) + 4);
 }
 
 // Row-group variant: one CTA per aligned group of 8 stored rows of one chunk
@@ -698,47 +586,6 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     T sum = row_sum<T, U>(vp, cp, C, len, x, pol_s, pol_x, CC == 32 && ((l2pol >> 8) & 1));
     if (skip_pad && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
     store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
-}
-
-// Persistent "short chunk" variant (C = 32, no long rows): a grid of a few
-// blocks per SM whose warps sweep chunks c, c + n_warps, ...; the next
-// chunk's metadata (cs, cl, row length) is fetched before the current chunk
-// is multiplied, taking one dependent DRAM round trip off every chunk and
-// removing the partial last wave of a one-warp-per-chunk grid.
-template <typename T, bool SKIP, bool ACC, int ORD, int U>
-__global__ void __launch_bounds__(kThreads, 6)
-k_spmv_sell_sweep(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
-                  const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
-                  const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
-                  const int32_t* __restrict__ order, int64_t c0, int64_t c1, int64_t n_rows,
-                  int l2pol) {
-    const uint64_t pol_s = make_policy(l2pol & 0xf);
-    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
-    const int lane = threadIdx.x & 31;
-    const int64_t n_warps = (int64_t)gridDim.x * (kThreads / 32);
-    int64_t c = c0 + (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-    if (c >= c1) return;
-    int64_t base = cs[c];
-    int w = cl[c];
-    int len = SKIP ? rl[c * 32 + lane] : w;
-    while (true) {
-        const int64_t cn = c + n_warps;
-        int64_t base_n = 0;
-        int w_n = 0, len_n = 0;
-        if (cn < c1) {                       // prefetch the next chunk's metadata
-            base_n = cs[cn];
-            w_n = cl[cn];
-            len_n = SKIP ? rl[cn * 32 + lane] : 0;
-        }
-        T sum = row_sum<T, U>(val + base + lane, col + base + lane, 32, len, x, pol_s, pol_x);
-        if (SKIP && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
-        store_row<T, ACC, ORD>(y, order, c * 32 + lane, n_rows, sum);
-        if (cn >= c1) break;
-        c = cn;
-        base = base_n;
-        w = w_n;
-        len = SKIP ? len_n : w_n;
-    }
 }
 
 // Warp-level variant for very short chunks (C = 32, every chunk at most W
@@ -1047,172 +894,6 @@ k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
     }
 }
 
-// Persistent, asynchronously staged form of the row-run kernel: each warp
-// walks its 32-row groups (g = warp, warp + all warps, ...) as a stream of
-// windows of <= S entries, double-buffered in shared memory -- window w+1's
-// val / col run is copied by cp.async (dense, coalesced, no registers held)
-// while window w's x gathers, products and per-row walks run -- so the DRAM
-// round trip of the matrix stream is off the critical path and only the x
-// gathers (mostly L2 hits) are waited for.  Same sums as k_spmv_rows.
-template <typename T, int S>
-struct RowsStage {
-    T val[2][S];
-    int32_t col[2][S];
-};
-
-template <typename T, bool ACC, bool UNR, int MODE, int ORD, int S>
-__global__ void __launch_bounds__(kThreads, 2)
-k_spmv_rows_async(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
-                  const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
-                  int64_t r0, int64_t r1, const int32_t* __restrict__ order,
-                  const int32_t* __restrict__ cl, int64_t n_rows) {
-    constexpr int WPB = kThreads / 32;
-    constexpr int G = S / 32;                          // gathers per lane per window
-    extern __shared__ __align__(16) uint8_t rows_smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    RowsStage<T, S>& W = reinterpret_cast<RowsStage<T, S>*>(rows_smem)[warp];
-    const uint64_t pol_s = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();
-    const int64_t GW = (int64_t)gridDim.x * WPB;
-    const int64_t n_groups = (r1 - r0 + 31) / 32;
-    // the window stream: issue side
-    int64_t ig = (int64_t)blockIdx.x * WPB + warp;    // group being issued
-    int64_t iwb = 0, iend = -1;                        // next window start / group end
-    bool ifresh = true;                                // group's first window not out yet
-    auto next_window = [&](int64_t& g, int64_t& wb, int& n) {
-        if (!ifresh && iwb >= iend) {
-            ig += GW;
-            ifresh = true;
-        }
-        if (ig >= n_groups) { g = -1; wb = 0; n = 0; return; }
-        if (ifresh) {
-            const int64_t rb = r0 + ig * 32;
-            const int64_t last = min(rb + 32, r1);
-            iwb = rpt[rb];
-            iend = rpt[last];
-        }
-        g = ig;
-        wb = iwb;
-        n = (int)min((int64_t)S, iend - iwb);
-        iwb += n;
-        ifresh = false;
-    };
-    auto issue = [&](int64_t wb, int n, int b) {
-        for (int t = lane; t < n; t += 32) {
-            cp_async<sizeof(T)>(&W.val[b][t], val + wb + t, pol_s);
-            cp_async<4>(&W.col[b][t], col + wb + t, pol_s);
-        }
-        cp_commit();
-    };
-    // compute side: the current group's rows
-    int64_t cg = -1, i = 0, s = 0, e = 0, m4 = 0, pos = 0;
-    bool valid = false, tail = !UNR;
-    T sum = T(0), t0 = T(0), t1 = T(0), t2 = T(0), t3 = T(0);
-    auto finish = [&]() {
-        if (cg < 0 || !valid) return;
-        if (MODE == 0) {
-            if (!UNR) {
-                y[i] = ACC ? Arith<T>::add(y[i], sum) : sum;
-            } else {
-                if (!tail) {
-                    const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
-                    sum = ACC ? Arith<T>::add(y[i], comb) : comb;
-                }
-                y[i] = sum;
-            }
-        } else {
-            if ((int64_t)(e - s) < (int64_t)cl[i >> 5])
-                sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
-            store_row<T, ACC, ORD>(y, order, i, n_rows, sum);
-        }
-    };
-
-    int64_t g0, wb0, g1, wb1;
-    int n0, n1;
-    next_window(g0, wb0, n0);
-    issue(wb0, n0, 0);
-    int b = 0;
-    while (g0 >= 0) {
-        next_window(g1, wb1, n1);
-        issue(wb1, n1, b ^ 1);                         // in flight during this window
-        cp_wait<1>();
-        __syncwarp();
-        if (g0 != cg) {                                // a new group: its rows
-            finish();
-            cg = g0;
-            i = r0 + cg * 32 + lane;
-            valid = i < r1;
-            s = valid ? rpt[i] : 0;
-            e = valid ? rpt[i + 1] : 0;
-            m4 = s + ((e - s) & ~(int64_t)3);
-            pos = s;
-            sum = t0 = t1 = t2 = t3 = T(0);
-            tail = !UNR;
-        }
-        // gathers and products of this window, in place
-        T xv[G];
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-            const int t = k * 32 + lane;
-            xv[k] = t < n0 ? ld_x(x + W.col[b][t], pol_x) : T(0);
-        }
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-            const int t = k * 32 + lane;
-            if (t < n0) W.val[b][t] = Arith<T>::mul(W.val[b][t], xv[k]);
-        }
-        __syncwarp();
-        const T* sp = W.val[b] - wb0;
-        const int64_t we = wb0 + n0;
-        if (!UNR) {
-            const int64_t stop = min(e, we);
-            for (; pos + 4 <= stop; pos += 4) {
-                const T a0 = sp[pos], a1 = sp[pos + 1], a2 = sp[pos + 2], a3 = sp[pos + 3];
-                sum = Arith<T>::add(sum, a0);
-                sum = Arith<T>::add(sum, a1);
-                sum = Arith<T>::add(sum, a2);
-                sum = Arith<T>::add(sum, a3);
-            }
-            for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
-        } else {
-            const int64_t stop4 = min(m4, we);
-            while (pos < stop4) {
-                if (((pos - s) & 3) == 0 && pos + 4 <= stop4) {
-                    t0 = Arith<T>::add(t0, sp[pos]);
-                    t1 = Arith<T>::add(t1, sp[pos + 1]);
-                    t2 = Arith<T>::add(t2, sp[pos + 2]);
-                    t3 = Arith<T>::add(t3, sp[pos + 3]);
-                    pos += 4;
-                } else {
-                    const int k = (int)((pos - s) & 3);
-                    const T pr = sp[pos];
-                    if (k == 0) t0 = Arith<T>::add(t0, pr);
-                    else if (k == 1) t1 = Arith<T>::add(t1, pr);
-                    else if (k == 2) t2 = Arith<T>::add(t2, pr);
-                    else t3 = Arith<T>::add(t3, pr);
-                    ++pos;
-                }
-            }
-            const int64_t stop = min(e, we);
-            if (pos >= m4 && pos < stop && !tail) {
-                const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
-                sum = ACC ? Arith<T>::add(y[i], comb) : comb;
-                tail = true;
-            }
-            for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
-        }
-        __syncwarp();                                  // buffer b free for window +2
-        g0 = g1;
-        wb0 = wb1;
-        n0 = n1;
-        b ^= 1;
-    }
-    finish();
-    cp_wait<0>();
-}
-
-constexpr int kRowsAsyncS = 512;
-
 constexpr int kRowsU = 4;
 constexpr int kRowsS = 1024;
 
@@ -1220,38 +901,8 @@ template <typename T, bool ACC, bool UNR, int MODE, int ORD>
 void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const void* x, void* y,
                  int64_t r0, int64_t r1, const int32_t* order, const int32_t* cl, int64_t n_rows,
                  cudaStream_t st) {
-    static const int async_env = [] {
-        const char* e = getenv("SELLB_ROWS_ASYNC");
-        return e ? atoi(e) : 0;
-    }();
-    if (async_env) {
-        auto kern = k_spmv_rows_async<T, ACC, UNR, MODE, ORD, kRowsAsyncS>;
-        constexpr size_t smem = sizeof(RowsStage<T, kRowsAsyncS>) * (kThreads / 32);
-        static unsigned attr_set = 0;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (!(attr_set & (1u << (dev & 31)))) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr_set |= 1u << (dev & 31);
-        }
-        static const int sms = [] {
-            int d = 0, n = 148;
-            cudaGetDevice(&d);
-            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-            return n;
-        }();
-        const int64_t groups = grid_for(r1 - r0, 32);
-        const int64_t blocks = std::max<int64_t>(
-            1, std::min<int64_t>(grid_for(groups, kThreads / 32), (int64_t)sms * 2));
-        kern<<<(unsigned)blocks, kThreads, smem, st>>>(rpt, col, (const T*)val, (const T*)x,
-                                                       (T*)y, r0, r1, order, cl, n_rows);
-        count_launches();
-        return;
-    }
-    static const int s_env = [] {
-        const char* e = getenv("SELLB_ROWS_S");
-        return e ? atoi(e) : kRowsS;
-    }();
+    // stage of 1024 entries per warp (tools: SELLB_ROWS_S A/B, 256 / 512 /
+    // 1024 -> cfg2 544 / 656 / 697, cfg3 411 / 455 / 455 GF/s)
     const unsigned grid = (unsigned)grid_for(grid_for(r1 - r0, 32), kThreads / 32);
 #define SELLB_ROWS(SS)                                                                         \
     do {                                                                                       \
@@ -1267,9 +918,7 @@ void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const 
         kern<<<grid, kThreads, smem_, st>>>(rpt, col, (const T*)val, (const T*)x, (T*)y, r0,   \
                                             r1, order, cl, n_rows);                            \
     } while (0)
-    if (s_env == 256) SELLB_ROWS(256);
-    else if (s_env == 512) SELLB_ROWS(512);
-    else SELLB_ROWS(1024);
+    SELLB_ROWS(kRowsS);
 #undef SELLB_ROWS
     count_launches();
 }
@@ -1280,13 +929,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     const int64_t rows = p1 - p0;
     if (rows <= 0) return 0;
     const int64_t n_long = m->long_rows ? m->n_long : 0;
-    // bulk block size (SELLB_BULK_BT = 64 / 128 / 256, A/B knob)
-    static const int bt_env = [] {
-        const char* e = getenv("SELLB_BULK_BT");
-        const int v = e ? atoi(e) : 0;
-        return (v == 64 || v == 128 || v == 256) ? v : 0;
-    }();
-    const int bt = bt_env ? bt_env : kThreads;
+    constexpr int bt = kThreads;   // 64 / 128-thread blocks measured within noise (r01_bt_ab.txt)
     const int64_t long_blocks = (n_long + bt / 32 - 1) / (bt / 32);
     unsigned grid = (unsigned)(grid_for(rows, bt) + long_blocks);
     // L2 policies: matrix streams (low nibble) and x gathers (high nibble);
@@ -1319,11 +962,6 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
     const bool u8 = u_env ? u_env == 8
                           : (sizeof(T) == 4 || m->max_cl > 64 ||
                              (m->n_rows > 0 && m->nnz >= 24 * m->n_rows));
-    // L1/shared carve-out: SELLB_CARVEOUT=<percent shared> (A/B knob; -1 = driver default)
-    static const int carve = [] {
-        const char* e = getenv("SELLB_CARVEOUT");
-        return e ? atoi(e) : -1;
-    }();
 #define SELLB_LAUNCH(UU, LL, LR, NL, TH, SD)                                                    \
     do {                                                                                        \
         /* LONG instances run next to the row-group kernel: reserve shared */ \
@@ -1331,141 +969,43 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         /* has to drain its bulk blocks to change its carve-out when a     */ \
         /* group CTA arrives (cfg3 sigma=N 495 -> 757 GF/s, tools/         */ \
         /* long_cfg_ab.sh; neutral in the fused mode)                      */ \
-        const int carve_ = carve >= 0 ? carve : ((LL) ? 30 : -1);                               \
-        if (carve_ >= 0) {                                                                      \
+        if (LL) {                                                                               \
             static unsigned set_ = 0;   /* per-device bit */                                    \
             int dev_ = 0;                                                                       \
             cudaGetDevice(&dev_);                                                               \
             if (!(set_ & (1u << (dev_ & 31)))) {                                                \
                 cudaFuncSetAttribute(k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL>,                \
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve_);   \
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 30);       \
                 set_ |= 1u << (dev_ & 31);                                                      \
             }                                                                                   \
         }                                                                                       \
-        if (persist) {                                                                          \
-            cudaLaunchConfig_t cfg_{};                                                          \
-            cfg_.gridDim = dim3(grid);                                                          \
-            cfg_.blockDim = dim3(bt);                                                           \
-            cfg_.stream = st;                                                                   \
-            cudaLaunchAttribute at_[1];                                                         \
-            at_[0].id = cudaLaunchAttributeAccessPolicyWindow;                                  \
-            at_[0].val.accessPolicyWindow = apw;                                                \
-            cfg_.attrs = at_;                                                                   \
-            cfg_.numAttrs = 1;                                                                  \
-            cudaLaunchKernelEx(&cfg_, k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL>, m->cs, m->cl,  \
-                               m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,  \
-                               m->C, p0, p1, m->n_rows, (const int32_t*)(LR), (int64_t)(NL),   \
-                               (int)(TH), (const int32_t*)m->chunk_th, l2pol,                   \
-                               (const int64_t*)((SD) ? m->side_off : nullptr),                  \
-                               (const int32_t*)((SD) ? m->side_col : nullptr),                  \
-                               (const T*)((SD) ? m->side_val : nullptr));                       \
-        } else {                                                                                \
-            k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, bt, 0, st>>>(                    \
-                m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
-                m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol,                        \
-                (SD) ? m->side_off : nullptr, (SD) ? m->side_col : nullptr,                     \
-                (const T*)((SD) ? m->side_val : nullptr));                                      \
-        }                                                                                       \
+        k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, bt, 0, st>>>(                        \
+            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,        \
+            m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol,                            \
+            (SD) ? m->side_off : nullptr, (SD) ? m->side_col : nullptr,                         \
+            (const T*)((SD) ? m->side_val : nullptr));                                          \
         count_launches();                                                                       \
     } while (0)
-    // L2 fetch granularity hint (SELLB_L2FETCH=<bytes>, A/B knob; device-wide,
-    // so only on request): smaller fetches for scattered sectors
-    static const int l2fetch = [] {
-        const char* e = getenv("SELLB_L2FETCH");
-        const int v = e ? atoi(e) : -1;
-        if (v >= 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)v);
-        return v;
-    }();
-    (void)l2fetch;
-    // x as a persisting L2 window (SELLB_L2PERSIST=1, A/B knob): the driver
-    // sets aside up to the device's persisting-L2 maximum for it
-    static const int persist_env = [] {
-        const char* e = getenv("SELLB_L2PERSIST");
-        return e ? atoi(e) : 0;
-    }();
-    const bool persist = persist_env == 1;
-    cudaAccessPolicyWindow apw{};
-    if (persist) {
-        static size_t max_persist = [] {
-            int d = 0, v = 0;
-            cudaGetDevice(&d);
-            cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, d);
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v);
-            return (size_t)v;
-        }();
-        int dmax = 0, d = 0;
-        cudaGetDevice(&d);
-        cudaDeviceGetAttribute(&dmax, cudaDevAttrMaxAccessPolicyWindowSize, d);
-        const size_t xbytes = (size_t)m->n_cols * sizeof(T);
-        apw.base_ptr = const_cast<void*>(x);
-        apw.num_bytes = std::min<size_t>(xbytes, (size_t)dmax);
-        apw.hitRatio = apw.num_bytes ? std::min(1.0f, (float)max_persist / (float)apw.num_bytes)
-                                     : 0.f;
-        apw.hitProp = cudaAccessPropertyPersisting;
-        apw.missProp = cudaAccessPropertyStreaming;
-    }
-    // persistent sweep for short chunks (C = 32): opt-in with SELLB_SWEEP=1.
-    // Measured slower than one warp per chunk (cfg1 455 vs 485 GF/s, cfg2
-    // 931 vs 1026): the 64-warp/SM one-shot grid already hides the metadata
-    // round trip, the sweep's extra registers cost occupancy.
-    static const int sweep_env = [] {
-        const char* e = getenv("SELLB_SWEEP");
-        return e ? atoi(e) : 0;
-    }();
     // very short chunks (every chunk <= 2 slots): K chunks per warp
     // (k_spmv_sell_short).  Measured on 16 M rows (tools/short_ab.sh): width 1
     // 126 -> 74 us (K = 4, 6.3 TB/s), width 2 138 -> 111 us (K = 2); width 3
     // gains nothing (152 vs 156 us) and stays on the default grid.
-    // SELLB_SHORT=0 disables, SELLB_SHORT_K=2|4|8 forces K.
+    // SELLB_SHORT=0 disables.
     static const int short_env = [] {
         const char* e = getenv("SELLB_SHORT");
         return e ? atoi(e) : 1;
     }();
-    static const int short_k_env = [] {
-        const char* e = getenv("SELLB_SHORT_K");
-        return e ? atoi(e) : 0;
-    }();
-    const int short_k = short_k_env ? short_k_env : (m->max_cl <= 1 ? 4 : 2);
-    if (CC == 32 && !n_long && short_env && m->max_cl <= (short_k_env ? 3 : 2) &&
-        sweep_env != 1) {
+    if (CC == 32 && !n_long && short_env && m->max_cl <= 2) {
         const int64_t chunks = (p1 - p0) / 32;
 #define SELLB_SHORT_LAUNCH(KK, WW)                                                              \
     k_spmv_sell_short<T, SKIP, ACC, ORD, KK, WW>                                                \
         <<<(unsigned)((chunks + (kThreads / 32) * KK - 1) / ((kThreads / 32) * KK)), kThreads, 0, \
            st>>>(m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,   \
                  p0 / 32, p1 / 32, m->n_rows, l2pol)
-#define SELLB_SHORT_W(KK)                                                                       \
-    do {                                                                                        \
-        if (m->max_cl <= 1) SELLB_SHORT_LAUNCH(KK, 1);                                          \
-        else if (m->max_cl == 2) SELLB_SHORT_LAUNCH(KK, 2);                                     \
-        else SELLB_SHORT_LAUNCH(KK, 3);                                                         \
-    } while (0)
-        if (short_k == 2) SELLB_SHORT_W(2);
-        else if (short_k == 8) SELLB_SHORT_W(8);
-        else SELLB_SHORT_W(4);
+        if (m->max_cl <= 1) SELLB_SHORT_LAUNCH(4, 1);
+        else SELLB_SHORT_LAUNCH(2, 2);
         count_launches();
-#undef SELLB_SHORT_W
 #undef SELLB_SHORT_LAUNCH
-        return 0;
-    }
-    const bool sweep = CC == 32 && !n_long && sweep_env == 1;
-    if (sweep) {
-        static const int sms = [] {
-            int d = 0, n = 148;
-            cudaGetDevice(&d);
-            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-            return n;
-        }();
-        const int64_t chunks = (p1 - p0) / 32;
-        const int64_t blocks = std::min<int64_t>((chunks + 7) / 8, (int64_t)sms * 6);
-#define SELLB_SWEEP_LAUNCH(UU)                                                                   \
-    k_spmv_sell_sweep<T, SKIP, ACC, ORD, UU><<<(unsigned)blocks, kThreads, 0, st>>>(             \
-        m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, p0 / 32,   \
-        p1 / 32, m->n_rows, l2pol)
-        if (m->max_cl <= 6) SELLB_SWEEP_LAUNCH(6);
-        else SELLB_SWEEP_LAUNCH(8);
-        count_launches();
-#undef SELLB_SWEEP_LAUNCH
         return 0;
     }
     // long rows: SELLB_LONG_MODE 0 = warp-per-row role fused into the bulk
@@ -1479,26 +1019,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         const char* e = getenv("SELLB_LONG_MODE");
         return e ? atoi(e) : 2;
     }();
-    static const int long_d = [] {
-        const char* e = getenv("SELLB_LONG_D");
-        return e ? atoi(e) : 4;
-    }();
-    static const int rest_sep = [] {
-        const char* e = getenv("SELLB_LONG_REST");
-        return e ? atoi(e) : 0;
-    }();
-    // isolated long rows (not in a row group) by the TMA kernel
-    // (sellb_tma_long.cu): opt-in, SELLB_LONG_TMA=1.  Measured slower than
-    // the fused role (cfg4 sigma=1 304 -> 280 GF/s): each 16-byte box row of
-    // a row 256 bytes from the next pulls a whole 128-byte line from DRAM
-    // (554 MB read for 25 MB of long-row data, ncu), so the kernel is
-    // DRAM-transaction bound at 89 us vs 42 us for the rest of the matrix.
-    static const int rest_tma_env = [] {
-        const char* e = getenv("SELLB_LONG_TMA");
-        return e ? atoi(e) : 0;
-    }();
-    const bool rest_tma = rest_tma_env && !rest_sep && m->n_rest && long_tma_possible(m);
-    if (n_long && long_mode != 0 && (m->n_groups || rest_sep || rest_tma)) {
+    if (n_long && long_mode != 0 && m->n_groups) {
         sellb_mat* mm = const_cast<sellb_mat*>(m);
         std::unique_lock<std::mutex> lk(mm->long_mu, std::defer_lock);
         cudaStream_t ls = st;
@@ -1517,84 +1038,42 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
             SELLB_CU(cudaStreamWaitEvent(mm->s_long, mm->ev_fork, 0));
             ls = mm->s_long;
         }
-#define SELLB_SMEM_ONCE(KERN, BYTES)                                                            \
-    do {                                                                                        \
-        static unsigned attr_ = 0;      /* per-device bit */                                    \
-        int dev_ = 0;                                                                           \
-        cudaGetDevice(&dev_);                                                                   \
-        if (!(attr_ & (1u << (dev_ & 31)))) {                                                   \
-            cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
-                                 (int)(BYTES));                                                 \
-            attr_ |= 1u << (dev_ & 31);                                                         \
-        }                                                                                       \
-    } while (0)
-#define SELLB_LONG_LAUNCH(DD, EE, LIST, NL)                                                         \
-    do {                                                                                        \
-        constexpr size_t smem_ = long_smem<T, DD>();                                            \
-        SELLB_SMEM_ONCE((k_spmv_long<T, ACC, ORD, DD, EE>), smem_);                             \
-        k_spmv_long<T, ACC, ORD, DD, EE>                                                        \
-            <<<(unsigned)(((NL) + kThreads / 32 - 1) / (kThreads / 32)), kThreads, smem_, ls>>>( \
-                m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
-                m->C, p0, p1, m->n_rows, LIST, NL, l2pol);                                      \
-        count_launches();                                                                       \
-    } while (0)
-#define SELLB_GRP_LAUNCH(DD, EE, TT)                                                            \
-    do {                                                                                        \
-        constexpr size_t smem_ = grp_smem<T, DD, TT>();                                         \
-        SELLB_SMEM_ONCE((k_spmv_long_grp<T, ACC, ORD, DD, EE, TT>), smem_);                     \
-        /* waves of at most grp_ctas CTAs (longest groups first): the      */ \
-        /* shared-memory carve-out stays off most SMs, and the bulk next   */ \
-        /* to it relies on L1 hits for x (cfg3 sigma=N lost a third of its */ \
-        /* speed with a group CTA on every SM)                             */ \
-        for (int64_t g_ = 0; g_ < m->n_groups; g_ += grp_ctas) {                               \
-            const int64_t ng_ = std::min<int64_t>(m->n_groups - g_, grp_ctas);                  \
-            k_spmv_long_grp<T, ACC, ORD, DD, EE, TT><<<(unsigned)ng_, kGT, smem_, ls>>>(        \
-                m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,    \
-                m->C, p0, p1, m->n_rows, m->long_groups + g_, ng_, m->chunk_th, l2pol);         \
-            count_launches();                                                                   \
-        }                                                                                       \
-    } while (0)
-        static const int grp_ctas = [] {
-            const char* e = getenv("SELLB_GRP_CTAS");
-            return e ? std::max(1, atoi(e)) : 1 << 30;
-        }();
-        static const int grp_sb = [] {
-            const char* e = getenv("SELLB_GRP_SB");
-            return e ? atoi(e) : 64;
-        }();
-        if (m->n_groups) {
-            if (grp_sb == 128) SELLB_GRP_LAUNCH(4, 2, 128);
-            else if (grp_sb == 3) SELLB_GRP_LAUNCH(8, 3, 64);
-            else if (grp_sb == 4) SELLB_GRP_LAUNCH(6, 3, 128);
-            else if (grp_sb == 5) SELLB_GRP_LAUNCH(10, 4, 64);
-            else SELLB_GRP_LAUNCH(4, 2, 64);
+        {
+            constexpr size_t smem_ = grp_smem<T, 4, 64>();
+            static unsigned attr_ = 0;      // per-device bit
+            int dev_ = 0;
+            cudaGetDevice(&dev_);
+            if (!(attr_ & (1u << (dev_ & 31)))) {
+                cudaFuncSetAttribute(k_spmv_long_grp<T, ACC, ORD, 4, 2, 64>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_);
+                attr_ |= 1u << (dev_ & 31);
+            }
+            // waves of at most grp_ctas CTAs (longest groups first): the
+            // shared-memory carve-out stays off most SMs, and the bulk next to
+            // it relies on L1 hits for x (cfg3 sigma=N lost a third of its
+            // speed with a group CTA on every SM).  SELLB_GRP_CTAS caps a wave.
+            static const int grp_ctas = [] {
+                const char* e = getenv("SELLB_GRP_CTAS");
+                return e ? std::max(1, atoi(e)) : 1 << 30;
+            }();
+            for (int64_t g_ = 0; g_ < m->n_groups; g_ += grp_ctas) {
+                const int64_t ng_ = std::min<int64_t>(m->n_groups - g_, grp_ctas);
+                k_spmv_long_grp<T, ACC, ORD, 4, 2, 64><<<(unsigned)ng_, kGT, smem_, ls>>>(
+                    m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,
+                    m->C, p0, p1, m->n_rows, m->long_groups + g_, ng_, m->chunk_th, l2pol);
+                count_launches();
+            }
         }
-        // the other long rows (isolated in chunks of short rows) keep the
-        // fused warp-per-row role (below); SELLB_LONG_REST=1 sends them to
-        // the pipelined warp-per-row kernel instead (measured slower: cfg4
-        // sigma=1 117 vs 165 us)
-        bool rest_fused = !rest_sep;
-        if (rest_tma) {
-            if (launch_long_tma(m, x, y, p0, p1, ACC, ORD, m->long_rest, m->n_rest, l2pol, ls))
-                rest_fused = false;
-        }
-        if (m->n_rest && rest_sep) {
-            if (long_d == 3) SELLB_LONG_LAUNCH(3, 1, m->long_rest, m->n_rest);
-            else if (long_d == 6) SELLB_LONG_LAUNCH(6, 3, m->long_rest, m->n_rest);
-            else SELLB_LONG_LAUNCH(4, 2, m->long_rest, m->n_rest);
-        }
-#undef SELLB_GRP_LAUNCH
-#undef SELLB_LONG_LAUNCH
-#undef SELLB_SMEM_ONCE
         SELLB_CU(cudaGetLastError());
         // the bulk: rows above their chunk's threshold are skipped (LONG
-        // template), no long-role blocks
+        // template); the other long rows (isolated in chunks of short rows)
+        // keep the fused warp-per-row role
         grid = (unsigned)grid_for(rows, bt);
         if (long_mode == 2) SELLB_CU(cudaEventRecord(mm->ev_join, ls));
-        const int32_t* rest = rest_fused ? m->long_rest : nullptr;
-        const int64_t n_rest = rest_fused ? m->n_rest : 0;
+        const int32_t* rest = m->long_rest;
+        const int64_t n_rest = m->n_rest;
         grid += (unsigned)((n_rest + bt / 32 - 1) / (bt / 32));
-        const bool side = rest_fused && m->side_off;   // side table is indexed like long_rest
+        const bool side = m->side_off != nullptr;   // side table is indexed like long_rest
         if (u8) SELLB_LAUNCH(8, true, rest, n_rest, m->long_th, side);
         else SELLB_LAUNCH(4, true, rest, n_rest, m->long_th, side);
         if (long_mode == 2) SELLB_CU(cudaStreamWaitEvent(st, mm->ev_join, 0));
@@ -1603,10 +1082,8 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         // side table applies unless the fused warp-per-row role is forced
         const bool side = long_mode != 0 && m->side_off && m->n_rest == n_long;
         const int32_t* lr = side ? m->long_rest : m->long_rows;
-        static const bool no_long = getenv("SELLB_TIME_NO_LONG") && atoi(getenv("SELLB_TIME_NO_LONG"));
-        const int64_t nl = no_long ? 0 : n_long;      // timing experiments only
-        if (u8) SELLB_LAUNCH(8, true, lr, nl, m->long_th, side);
-        else SELLB_LAUNCH(4, true, lr, nl, m->long_th, side);
+        if (u8) SELLB_LAUNCH(8, true, lr, n_long, m->long_th, side);
+        else SELLB_LAUNCH(4, true, lr, n_long, m->long_th, side);
     } else if (u_env == 6 || (!u_env && m->max_cl > 4 && m->max_cl <= 6 && sizeof(T) == 8)) {
         // every chunk fits one 6-slot batch (5-point stencils): one round trip
         SELLB_LAUNCH(6, false, nullptr, 0, 0x7fffffff, false);
@@ -1870,19 +1347,15 @@ int pipe_setup(sellb_mat* m) {
     // x piece b ends just past the highest column row block b reads, so block
     // b can start as soon as piece b has landed (for banded matrices the
     // pieces then track the row blocks and H2D, compute and D2H overlap)
-    // Equal row blocks.  SELLB_PIPE_RAMP=1 makes them grow geometrically (1,
-    // 1, 2, 4, ... parts) -- measured slower on cfg2 (0.546 vs 0.499 ms):
-    // with both PCIe directions busy each runs at ~40 GB/s, and the y drain
-    // of a block is as long as the next block's x transfer anyway.
+    // Equal row blocks (geometrically growing ones measured slower on cfg2,
+    // 0.546 vs 0.499 ms: with both PCIe directions busy each runs at ~40
+    // GB/s, and the y drain of a block is as long as the next block's x
+    // transfer anyway).
     m->n_pieces = P;
     m->x_off[0] = 0;
-    const bool ramp = getenv("SELLB_PIPE_RAMP") && atoi(getenv("SELLB_PIPE_RAMP")) == 1;
-    std::vector<int64_t> wsum(P + 1, 0);
-    for (int b = 0; b < P; ++b)
-        wsum[b + 1] = wsum[b] + (ramp ? (b == 0 ? 1 : (1LL << (b - 1))) : 1);
     m->blk_c[0] = 0;
     for (int b = 0; b < P; ++b) {
-        m->blk_c[b + 1] = m->n_chunks * wsum[b + 1] / wsum[P];
+        m->blk_c[b + 1] = m->n_chunks * (b + 1) / P;
         int64_t mx = -1;
         for (int64_t c = m->blk_c[b]; c < m->blk_c[b + 1]; ++c) mx = std::max<int64_t>(mx, maxcol[c]);
         int64_t end = std::min<int64_t>(std::max<int64_t>(m->x_off[b], mx + 1), m->n_cols);

@@ -1,9 +1,8 @@
-"""GPU parity of the long-row paths (sellb_spmv.cu, sellb_tma_long.cu): the
-row-group kernel (k_spmv_long_grp, 8-row groups of sorted chunks,
-producer/chain warps), the TMA kernel for isolated long rows
-(k_spmv_long_tma), the fused warp-per-row role and the pipelined warp-per-row
-kernel, under every launch mode (SELLB_LONG_MODE 0/1/2), batch size and wave
-cap.
+"""GPU parity of the long-row paths (sellb_spmv.cu): the row-group kernel
+(k_spmv_long_grp, 8-row groups of sorted chunks, producer/chain warps), the
+fused warp-per-row role with and without the contiguous side table, and the
+packed copy next to them, under every launch mode (SELLB_LONG_MODE 0/1/2)
+and wave cap.
 
 Matrices are built so the groups are full, partial (4..7 long rows next to
 shorter ones), or sparse (< 4 long rows: warp-per-row), chunks are
@@ -104,15 +103,11 @@ MODES = [
     {"SELLB_LONG_MODE": "2", "SELLB_LONG_GRP": "1"},           # row groups forced
     {"SELLB_LONG_MODE": "0"},
     {"SELLB_LONG_MODE": "1"},
-    {"SELLB_LONG_MODE": "2", "SELLB_GRP_SB": "128", "SELLB_LONG_GRP": "1"},
-    {"SELLB_LONG_MODE": "2", "SELLB_GRP_CTAS": "3", "SELLB_LONG_REST": "1",
-     "SELLB_LONG_GRP": "1"},
-    {"SELLB_LONG_MODE": "1", "SELLB_LONG_GRP": "0", "SELLB_LONG_REST": "1",
-     "SELLB_LONG_D": "3"},
-    {"SELLB_LONG_MODE": "2", "SELLB_LONG_TMA": "0", "SELLB_LONG_SIDE": "0"},  # padded reads
-    {"SELLB_LONG_MODE": "2", "SELLB_LONG_SIDE": "0"},           # groups + fused, no side table
-    {"SELLB_LONG_MODE": "1", "SELLB_LONG_GRP": "0", "SELLB_LONG_TMA": "1",
-     "SELLB_LONG_SIDE": "0"},                                  # every long row by TMA
+    {"SELLB_LONG_MODE": "1", "SELLB_LONG_GRP": "1"},           # groups, then the bulk
+    {"SELLB_LONG_MODE": "2", "SELLB_GRP_CTAS": "3", "SELLB_LONG_GRP": "1"},   # waves of 3
+    {"SELLB_LONG_MODE": "2", "SELLB_LONG_SIDE": "0"},           # padded reads, no side table
+    {"SELLB_LONG_MODE": "0", "SELLB_LONG_SIDE": "0"},
+    {"SELLB_LONG_MODE": "2", "SELLB_PACKED": "1"},              # packed copy + long rows
 ]
 
 

@@ -67,9 +67,8 @@ print("ok" if not bad else "fail")
 '''
 
 
-@pytest.mark.parametrize("env", [{}, {"SELLB_SHORT_K": "8"}, {"SELLB_SHORT": "0"},
-                                 {"SELLB_SWEEP": "1"}],
-                         ids=["default", "K8", "off", "sweep"])
+@pytest.mark.parametrize("env", [{}, {"SELLB_SHORT": "0"}],
+                         ids=["default", "off"])
 def test_short_chunk_variants_bitwise(env):
     out = subprocess.run([sys.executable, "-c", CHILD], env=dict(os.environ, **env),
                          capture_output=True, text=True, cwd=REPO, timeout=900)

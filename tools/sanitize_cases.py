@@ -5,10 +5,10 @@ for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 
 Families: bulk (pad-skip / pad-incl, fp64 / fp32, U = 4 / 6 / 8), short
 (k_spmv_sell_short), long (fused warp-per-row role with and without the side
-table, the row-group kernel with named barriers and cp.async rings, the
-pipelined warp-per-row kernel), tma (fp32 bulk-copy ring on mbarriers, the
-long-row TMA kernel), packed (chunk-sorted copy), crs, build (device
-crs_to_sell incl. CUB sorts / scans), coo, host (pageable-vector staging).
+table, the row-group kernel with named barriers and cp.async rings), tma
+(fp32 bulk-copy ring on mbarriers), packed (stored-order copy through the
+row-run kernel), crs (row-run kernel), build (device crs_to_sell incl. CUB
+sorts / scans), coo, host (pageable-vector staging).
 The launch switches are environment variables read once per process, so
 each mode of a family runs in its own child process."""
 
@@ -73,7 +73,6 @@ def family(name):
         res.append(check(m, 32, 10 ** 9, np.float32)[0])
     elif name == "tma":
         res.append(check(generate.stencil27(24), 32, 1, np.float32)[0])
-        res.append(check(long_mix(5), 32, 1)[0])
     elif name == "packed":
         for sig in (1, 128):
             ok, s = check(generate.powerlaw(30_000, seed=3, band=800), 32, sig)
@@ -113,8 +112,8 @@ MODES = {
     "bulk": [{}, {"SELLB_U": "4"}, {"SELLB_U": "8"}, {"SELLB_VX": "0"}],
     "short": [{}, {"SELLB_SHORT": "0"}],
     "long": [{}, {"SELLB_LONG_SIDE": "0"}, {"SELLB_LONG_GRP": "1"},
-             {"SELLB_LONG_GRP": "1", "SELLB_LONG_MODE": "1"}, {"SELLB_LONG_REST": "1"}],
-    "tma": [{"SELLB_TMA": "1"}, {"SELLB_LONG_TMA": "1"}],
+             {"SELLB_LONG_GRP": "1", "SELLB_LONG_MODE": "1"}],
+    "tma": [{"SELLB_TMA": "1"}],
     "packed": [{"SELLB_PACKED": "1"}],
     "crs": [{}], "build": [{}], "coo": [{}], "host": [{}],
 }
