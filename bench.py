@@ -429,13 +429,30 @@ def host_workload(args, dt_np):
                 "value_1thread": round(gf1, 4),
                 "sample": sample + f"; host {host_cpu_desc()}"}
 
+    b = build_roofline(s.info(), dt_np, build_dev_ms, build_s,
+                       note="device_ms: crs_to_sell on CRS already in HBM (CUDA events); "
+                            "host_s adds the pageable H2D of the CRS; cpu: the C "
+                            "restatement of formats.py:295-393 (oracle), one thread")
+    b["cpu_port_1thread_s"] = round(build_cpu_s, 4)
     return {"sell": s, "desc": desc, "x": x, "build_s": build_s, "parity": parity, "cpu": cpu,
-            "build": {"device_ms": round(build_dev_ms, 3),
-                      "host_to_sell_s": round(build_s, 4),
-                      "cpu_port_1thread_s": round(build_cpu_s, 4),
-                      "note": "device_ms: crs_to_sell on CRS already in HBM (CUDA events); "
-                              "host_to_sell_s adds the pageable H2D of the CRS; cpu: the C "
-                              "restatement of formats.py:295-393 (oracle), one thread"}}
+            "build": b}
+
+
+def build_roofline(info, dt_np, device_ms, host_s, note=""):
+    """Bytes the device build (crs_to_sell, formats.py:295-393) must move at
+    least -- read the CRS, write the SELL arrays (cs, cl, col, val,
+    row_lengths, perm, order) -- against its CUDA-event time."""
+    s_v = 4 if dt_np == np.float32 else 8
+    n, n_pad, nch = info.n_rows, info.n_rows_padded, info.n_chunks
+    nnz, slots = info.nnz, info.slots
+    read = 8 * (n + 1) + (4 + s_v) * nnz
+    write = 12 * nch + 8 + (4 + s_v) * slots + 4 * n_pad + 4 * n + 4 * n_pad
+    gbs = (read + write) / (device_ms / 1e3) / 1e9 if device_ms > 0 else None
+    peak, _ = measured_peaks()
+    return {"device_ms": round(device_ms, 3), "host_s": round(host_s, 4),
+            "bytes_alg": int(read + write),
+            "achieved_gbs": round(gbs, 1) if gbs else None,
+            "frac_of_hbm": round(gbs / peak, 4) if gbs else None, "note": note}
 
 
 def parity_blocks(n, blk):
@@ -464,12 +481,21 @@ def cfg5_workload(args, dt_np):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rpt, col, val = generate.hamiltonian_device(n, device=0, dtype=dt_np)
+    torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
     s = sb.crs_to_sell_device(rpt, col, val, n, n, args.C, sigma)
-    del rpt, col, val
     torch.cuda.synchronize()
-    torch.cuda.empty_cache()
     build_s = time.perf_counter() - t0 - t_gen
+    # the device build alone, timed with CUDA events (a second build of the
+    # same CRS, freed at once)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sb.crs_to_sell_device(rpt, col, val, n, n, args.C, sigma).free()
+    e1.record()
+    e1.synchronize()
+    build_dev_ms = e0.elapsed_time(e1)
+    del rpt, col, val
+    torch.cuda.empty_cache()
     x = np.random.default_rng(12345).uniform(-1, 1, n).astype(dt_np)
     blk = 1 << 16
 
@@ -500,7 +526,12 @@ def cfg5_workload(args, dt_np):
 
     scope = (f"{len(parity_blocks(n, blk))} blocks of {blk} rows (first, last, quarter "
              f"boundaries): cs/cl/col/val/row_lengths and y bit-exact vs the oracle")
+    info = s.info()
     return {"sell": s, "parity_scope": scope,
+            "build": build_roofline(info, dt_np, build_dev_ms, build_s,
+                                    note="device_ms: crs_to_sell_device on the device-"
+                                         "generated CRS (CUDA events); generation "
+                                         f"{t_gen:.3f} s"),
             "desc": f"banded-random Hamiltonian-like N={n} (device-generated, "
                                f"generation {t_gen:.2f} s)",
             "x": x, "build_s": build_s, "parity": parity, "cpu": cpu}

@@ -262,6 +262,16 @@ int sellb_gen_hamiltonian_fill(int64_t n, int64_t r0, int64_t r1, const int64_t*
                                int32_t n_off, double keep, uint64_t seed, const int64_t* rpt_dev,
                                int32_t* col_dev, void* val_dev, int32_t dtype, void* stream);
 
+/* cfg3 generator (BASELINE configs[2]) straight into device CRS, rows
+ * [r0, r1) of the N = n power-law matrix (generate.py:powerlaw_rows, the
+ * same counter-hash definition, bit-identical): rpt first (returns nnz),
+ * then col / val into caller buffers. */
+int sellb_gen_powerlaw_rpt(int64_t n, int64_t r0, int64_t r1, double base, int64_t lmax,
+                           uint64_t seed, int64_t* rpt_dev, int64_t* nnz_out, void* stream);
+int sellb_gen_powerlaw_fill(int64_t n, int64_t r0, int64_t r1, double base, int64_t lmax,
+                            int64_t band, uint64_t seed, const int64_t* rpt_dev, int32_t* col_dev,
+                            void* val_dev, int32_t dtype, void* stream);
+
 /* COO -> canonical CRS on the device: the step before the build
  * (SURVEY.md §8(f)3).  Replaces COOMatrix's bounds check (formats.py:50-70),
  * canonicalize_coo (formats.py:89-108) and coo_to_crs (formats.py:169-175).

@@ -38,7 +38,7 @@ EXPORTED = (
     "sellb_launch_count", "sellb_long_info", "sellb_streamed_bytes",
     "sellb_lru_stream_misses", "sellb_sell_x_lines", "sellb_host_register",
     "sellb_host_unregister", "sellb_set_packed", "sellb_crs_import", "sellb_crs_spmv_host",
-    "sellb_crs_free",
+    "sellb_crs_free", "sellb_gen_powerlaw_rpt", "sellb_gen_powerlaw_fill",
 )
 
 
@@ -109,6 +109,10 @@ _PROTOS = {
     "sellb_gen_hamiltonian_fill": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i32, ctypes.c_double,
                                                   ctypes.c_uint64, _vp, _vp, _vp, _i32, _vp]),
     "sellb_host_free": (ctypes.c_int, [_vp]),
+    "sellb_gen_powerlaw_rpt": (ctypes.c_int, [_i64, _i64, _i64, ctypes.c_double, _i64,
+                                              ctypes.c_uint64, _vp, ctypes.POINTER(_i64), _vp]),
+    "sellb_gen_powerlaw_fill": (ctypes.c_int, [_i64, _i64, _i64, ctypes.c_double, _i64, _i64,
+                                               ctypes.c_uint64, _vp, _vp, _vp, _i32, _vp]),
     "sellb_host_register": (ctypes.c_int, [_vp, ctypes.c_size_t]),
     "sellb_host_unregister": (ctypes.c_int, [_vp]),
     "sellb_export_range": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),

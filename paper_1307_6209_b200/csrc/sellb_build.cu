@@ -600,14 +600,17 @@ namespace sellb {
 // bulk role, and the model leaves them there)
 int build_packed(sellb_mat* m, cudaStream_t st, int force) {
     free_packed(m);
+    bool from_env = false;
     if (force == -2) {
         const char* e = getenv("SELLB_PACKED");
         force = (!e || strcmp(e, "auto") == 0) ? -1 : (atoi(e) ? 1 : 0);
+        from_env = true;
     }
     if (force == 0) return 0;
     const bool possible = m->C == 32 && m->rl && m->n_chunks > 0 && m->slots > 0;
     if (!possible) {
-        if (force == 1)
+        // an explicit request fails loudly; SELLB_PACKED=1 applies where it can
+        if (force == 1 && !from_env)
             return set_error(SELLB_EPARAM, "the packed copy needs C = 32 and row_lengths");
         return 0;
     }

@@ -160,26 +160,73 @@ def _splitmix64(z):
     return z ^ (z >> np.uint64(31))
 
 
-def powerlaw(n=4_000_000, mean_base=10.0, lmax=4096, band=50_000, seed=3):
-    """cfg3: row lengths clip(floor(mean_base (1 + Pareto(2))), 1, lmax)
-    (mean ~20, zeta ~2); each row's columns are one contiguous window
-    starting at a hashed offset within +-band of the diagonal; values
-    uniform(-1, 1)."""
-    rng = np.random.default_rng(seed)
-    lmax = min(lmax, n)
-    lengths = np.clip(np.floor(mean_base * (1.0 + rng.pareto(2.0, n))), 1,
-                      lmax).astype(np.int64)
-    rows = np.arange(n, dtype=np.int64)
+_M64 = (1 << 64) - 1
+
+
+def _pl_lengths(rows, n, mean_base, lmax, seed):
+    su = np.uint64((seed * 0xA24BAED4963EE407) & _M64)
+    hu = _splitmix64(rows.astype(np.uint64) ^ su)
+    u = (hu >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    q = mean_base / np.sqrt(1.0 - u)
+    return np.clip(np.floor(q), 1, min(lmax, n)).astype(np.int64)
+
+
+def powerlaw_rows(n, r0, r1, mean_base=10.0, lmax=4096, band=50_000, seed=3):
+    """Rows [r0, r1) of the cfg3 power-law matrix, row-addressable (any
+    block regenerates alone; the device generator, csrc/sellb_gen.cu
+    k_pl_*, is bit-identical).  Row i: length floor(mean_base / sqrt(1 - u_i))
+    clipped to [1, min(lmax, n)] with u_i a counter hash in [0, 1) -- the
+    inverse CDF of mean_base (1 + Pareto(2)), mean ~20, zeta ~2; columns one
+    contiguous window starting at a hashed offset within +-band of the
+    diagonal; values counter hashes mapped to [-1, 1), exact in fp64."""
+    rows = np.arange(r0, r1, dtype=np.int64)
+    lengths = _pl_lengths(rows, n, mean_base, lmax, seed)
     h = _splitmix64(rows.astype(np.uint64) ^ np.uint64(seed))
     start = rows + (h % np.uint64(2 * band + 1)).astype(np.int64) - band
-    start = np.clip(start, 0, n - lengths)
-    rpt = np.zeros(n + 1, dtype=np.int64)
+    start = np.clip(np.minimum(start, n - lengths), 0, None)
+    rpt = np.zeros(len(rows) + 1, dtype=np.int64)
     np.cumsum(lengths, out=rpt[1:])
     nnz = int(rpt[-1])
     k = np.arange(nnz, dtype=np.int64) - np.repeat(rpt[:-1], lengths)
     col = (np.repeat(start, lengths) + k).astype(np.int32)
-    val = rng.uniform(-1.0, 1.0, nnz)
+    rk = np.repeat(rows.astype(np.uint64) * np.uint64(0x100000001B3), lengths)
+    vh = _splitmix64(rk ^ (k.astype(np.uint64) +
+                           np.uint64((seed + 0x5851F42D4C957F2D) & _M64)))
+    val = (vh >> np.uint64(11)).astype(np.float64) * (2.0 / 9007199254740992.0) - 1.0
+    return rpt, col, val
+
+
+def powerlaw(n=4_000_000, mean_base=10.0, lmax=4096, band=50_000, seed=3):
+    """cfg3 (BASELINE configs[2]): N = 4M power-law rows, see powerlaw_rows."""
+    with np.errstate(over="ignore"):
+        rpt, col, val = powerlaw_rows(n, 0, n, mean_base, lmax, band, seed)
     return CRSMatrix(n, n, rpt, col, val)
+
+
+def powerlaw_device(n=4_000_000, r0=0, r1=None, mean_base=10.0, lmax=4096, band=50_000,
+                    seed=3, device=0, dtype=np.float64):
+    """Rows [r0, r1) of the cfg3 matrix generated ON the GPU (bit-identical to
+    powerlaw_rows).  Returns torch CUDA tensors (rpt, col, val)."""
+    import ctypes
+    import torch
+    from . import _lib
+    r1 = n if r1 is None else r1
+    lib = _lib.require_device()
+    dev = torch.device("cuda", device)
+    rpt = torch.empty(r1 - r0 + 1, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    nnz = ctypes.c_int64(0)
+    with torch.cuda.device(dev):
+        _lib.check(lib.sellb_gen_powerlaw_rpt(n, r0, r1, float(mean_base), int(lmax),
+                                              int(seed), rpt.data_ptr(), ctypes.byref(nnz), st))
+        f32 = np.dtype(dtype) == np.float32
+        col = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+        val = torch.empty(max(nnz.value, 1), dtype=torch.float32 if f32 else torch.float64,
+                          device=dev)
+        _lib.check(lib.sellb_gen_powerlaw_fill(
+            n, r0, r1, float(mean_base), int(lmax), int(band), int(seed), rpt.data_ptr(),
+            col.data_ptr(), val.data_ptr(), _lib.SELLB_F32 if f32 else _lib.SELLB_F64, st))
+    return rpt, col[: nnz.value], val[: nnz.value]
 
 
 # cfg5 hopping offsets: short bands plus long-range hops (|d| up to N/16);

@@ -327,6 +327,22 @@ def test_cfg5_generator_matches_numpy(n, r0, r1):
     assert val_d.cpu().numpy().tobytes() == val.tobytes()
 
 
+@pytest.mark.parametrize("n,r0,r1,kw", [
+    (4_000_000, 0, 4_000_000, {}),                        # the whole cfg3 matrix
+    (4_000_000, 1_234_567, 1_300_000, {}),                # a block
+    (200_000, 0, 200_000, {"seed": 4, "band": 5000}),
+    (5000, 0, 5000, {"lmax": 9000, "mean_base": 40.0}),   # rows capped at n
+])
+def test_cfg3_generator_matches_numpy(n, r0, r1, kw):
+    """Device power-law generator (csrc/sellb_gen.cu k_pl_*) == the NumPy
+    row-addressable definition (generate.powerlaw_rows), bit for bit."""
+    rpt_d, col_d, val_d = generate.powerlaw_device(n, r0, r1, **kw)
+    rpt, col, val = generate.powerlaw_rows(n, r0, r1, **kw)
+    assert rpt_d.cpu().numpy().tobytes() == rpt.tobytes()
+    assert col_d.cpu().numpy().tobytes() == col.tobytes()
+    assert val_d.cpu().numpy().tobytes() == val.tobytes()
+
+
 def test_cfg5_block_parity_small():
     """Device-generated, device-built matrix: sampled row blocks equal the
     oracle build of the same block regenerated on the host."""
