@@ -9,11 +9,11 @@ run() { name=$1; shift
 import json, sys
 try:
     d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
-    c, r = d["config"], d["roofline"]
+    c, r = d["details"], d["roofline"]
     cpu = (d.get("cpu_baseline") or {}).get("value")
     print(f"{sys.argv[1]:22} {d['value']:9.2f} GF/s frac {r['frac']:.3f} kern {r['kernel_ms']:.4f} ms "
-          f"beta {c.get('beta')} {c.get('kernel_variant')} parity {c.get('parity_vs_oracle')} "
-          f"e2e {d['e2e']['value']} cpu {cpu}")
+          f"beta {c.get('beta')} {c.get('kernel_variant')}{'+packed' if c.get('packed_copy') else ''} "
+          f"parity {c.get('parity_vs_oracle')} e2e {d['e2e']['value']} cpu {cpu}")
 except Exception as e:
     print(sys.argv[1], "FAILED", e)
 PY
@@ -30,5 +30,8 @@ for C in 8 16 32 64 128; do
   done
   run cfg4_C${C}_s$((16*C))_f32 --config cfg4 --C $C --sigma $((16*C)) --dtype f32 --steps 300 --warmup 10 --skip-cpu
 done
+export SELLB_PACKED=0   # the same layout through the SELL bulk role, for comparison
+run cfg3_s1_nopack      --config cfg3 --sigma 1 --steps 300 --warmup 10 --skip-cpu --skip-parity
+unset SELLB_PACKED
 run cfg5_s512           --config cfg5 --sigma 512 --steps 100 --warmup 5 --cpu-budget 4
 run cfg5_s1             --config cfg5 --sigma 1 --steps 100 --warmup 5 --skip-cpu
