@@ -87,7 +87,8 @@ int sellb_long_info(const sellb_mat* m, int64_t* n_long, int64_t* n_groups, int6
  * pad-inclusive chunks, the 32-byte (and 64-byte) sectors of bulk rows in
  * chunks read with pad-skip semantics, the long rows' entries (contiguous
  * side table, or one sector per element from the padded layout);
- * extra_bytes = the row_lengths reads. */
+ * extra_bytes = the row_lengths reads.  With the packed copy: (s_v + 4) per
+ * nonzero, extra = its row offsets and the chunk widths. */
 int sellb_streamed_bytes(const sellb_mat* m, int64_t* matrix_bytes, int64_t* matrix_bytes_64,
                          int64_t* extra_bytes, void* stream);
 

@@ -1195,6 +1195,15 @@ int sellb_streamed_bytes(const sellb_mat* m, int64_t* matrix_bytes, int64_t* mat
     DeviceGuard guard(m->device);
     cudaStream_t st = (cudaStream_t)stream;
     const int vs = (int)vsize(m->dtype);
+    if (m->pcol && m->variant == SELLB_VARIANT_PAD_SKIP) {
+        // the packed stored-order copy: every entry once, contiguous; plus
+        // the row offsets and the chunk widths (pad fix-up)
+        const int64_t mb = (int64_t)(vs + 4) * m->nnz;
+        if (matrix_bytes) *matrix_bytes = mb;
+        if (matrix_bytes_64) *matrix_bytes_64 = mb;
+        if (extra_bytes) *extra_bytes = 8 * (m->n_pad + 1) + 4 * m->n_chunks;
+        return 0;
+    }
     unsigned long long h[4] = {0, 0, 0, 0};
     const bool skip = m->variant == SELLB_VARIANT_PAD_SKIP;
     if (m->n_chunks && (m->rl || !skip)) {

@@ -6,7 +6,7 @@ ncu's dram__bytes_read.sum + dram__bytes_write.sum of the SpMV kernel.
 
 On the GPU box (one ncu pass, one SpMV launch per layout):
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-        -k regex:k_spmv_sell --csv --log-file gpurun_out/alpha.csv \
+        -k regex:"k_spmv_(sell|rows)" --csv --log-file gpurun_out/alpha.csv \
         python tools/alpha_sweep.py run gpurun_out/alpha_layouts.json
 and without ncu for timing:
     python tools/alpha_sweep.py time gpurun_out/alpha_times.json
@@ -58,7 +58,8 @@ def run(out_json, timed=False):
                "n_cols": info.n_cols, "n_pad": info.n_rows_padded, "n_chunks": info.n_chunks,
                "slots": info.slots, "beta": info.nnz / info.slots, "beta_eff": be,
                "val_sectors": vs, "col_sectors": cs, "val_sectors64": v64,
-               "col_sectors64": c64, "variant": s.variant}
+               "col_sectors64": c64,
+               "variant": s.variant + ("+packed" if s.packed else "")}
         if timed:
             for _ in range(5):
                 sb.spmv_sell(s, x, y)
