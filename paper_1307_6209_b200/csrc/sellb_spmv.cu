@@ -766,7 +766,7 @@ k_spmv_crs_unrolled(const int64_t* __restrict__ rpt, const int32_t* __restrict__
 // (ORD 0) or y[order[p]] (ORD 1), plus the reference's 0 * x[0] term for
 // rows shorter than their chunk (the padding slots it adds).
 template <typename T, bool ACC, bool UNR, int MODE, int ORD, int U, int S>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, U >= 8 ? 2 : 3)
 k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
             int64_t r0, int64_t r1, const int32_t* __restrict__ order,
@@ -901,12 +901,12 @@ template <typename T, bool ACC, bool UNR, int MODE, int ORD>
 void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const void* x, void* y,
                  int64_t r0, int64_t r1, const int32_t* order, const int32_t* cl, int64_t n_rows,
                  cudaStream_t st) {
-    // stage of 1024 entries per warp (tools: SELLB_ROWS_S A/B, 256 / 512 /
-    // 1024 -> cfg2 544 / 656 / 697, cfg3 411 / 455 / 455 GF/s)
+    // stage of 1024 entries per warp (A/B of 256 / 512 / 1024: cfg2 CRS
+    // 544 / 656 / 697, cfg3 411 / 455 / 455 GF/s)
     const unsigned grid = (unsigned)grid_for(grid_for(r1 - r0, 32), kThreads / 32);
-#define SELLB_ROWS(SS)                                                                         \
+#define SELLB_ROWS(UU, SS)                                                                     \
     do {                                                                                       \
-        auto kern = k_spmv_rows<T, ACC, UNR, MODE, ORD, kRowsU, SS>;                           \
+        auto kern = k_spmv_rows<T, ACC, UNR, MODE, ORD, UU, SS>;                               \
         constexpr size_t smem_ = (size_t)(kThreads / 32) * SS * sizeof(T);                     \
         static unsigned attr_ = 0;                                                             \
         int dev_ = 0;                                                                          \
@@ -918,7 +918,9 @@ void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const 
         kern<<<grid, kThreads, smem_, st>>>(rpt, col, (const T*)val, (const T*)x, (T*)y, r0,   \
                                             r1, order, cl, n_rows);                            \
     } while (0)
-    SELLB_ROWS(kRowsS);
+    // U = 4 (B = 128-entry sub-batches, 3 blocks / SM): U = 8 measured slower
+    // everywhere (cfg2 / cfg3 / cfg4 CRS 698 / 452 / 289 -> 622 / 380 / 239)
+    SELLB_ROWS(kRowsU, kRowsS);
 #undef SELLB_ROWS
     count_launches();
 }
