@@ -108,6 +108,7 @@ def _run_host_partitioned(run_range, n_units, threads, scheduling):
 # One-shot vectors never pay for the registration.
 
 _PIN_MIN_BYTES = 16 << 20
+_PIN_OFF = bool(__import__("os").environ.get("SELLB_NO_PIN"))   # A/B: staging only
 _pin_state = {}
 _pin_lock = threading.Lock()
 
@@ -131,7 +132,7 @@ def _unpin(key):
 
 def _pin_hint(a):
     """Register a host vector for DMA the second time it is seen."""
-    if a.nbytes < _PIN_MIN_BYTES:
+    if _PIN_OFF or a.nbytes < _PIN_MIN_BYTES:
         return
     own = _data_owner(a)
     if own is None:
