@@ -107,7 +107,7 @@ def _run_host_partitioned(run_range, n_units, threads, scheduling):
 # garbage-collected (weakref.finalize runs before NumPy frees the data).
 # One-shot vectors never pay for the registration.
 
-_PIN_MIN_BYTES = 16 << 20
+_PIN_MIN_BYTES = 1 << 20
 _PIN_OFF = bool(__import__("os").environ.get("SELLB_NO_PIN"))   # A/B: staging only
 _pin_state = {}
 _pin_lock = threading.Lock()
