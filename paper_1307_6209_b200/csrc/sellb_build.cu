@@ -687,6 +687,7 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
                          int32_t align_bytes, int32_t permute_cols, int32_t device, void* stream,
                          int32_t ptrs_on_device, sellb_mat** out) {
     clear_error();
+    NvtxRange nvtx_("sellb_build_from_crs");
     if (!out) return set_error(SELLB_EPARAM, "out must not be NULL");
     *out = nullptr;
     // parameter checks in the reference's order (formats.py:309-319)
@@ -908,6 +909,7 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
                  int32_t col_permuted, int32_t device, void* stream, int32_t ptrs_on_device,
                  sellb_mat** out) {
     clear_error();
+    NvtxRange nvtx_("sellb_import");
     if (!out) return set_error(SELLB_EPARAM, "out must not be NULL");
     *out = nullptr;
     if (C < 1) return set_error(SELLB_EPARAM, "chunk height C must be >= 1, got %d", C);

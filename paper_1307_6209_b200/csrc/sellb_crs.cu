@@ -82,6 +82,7 @@ int sellb_crs_import(const int64_t* rpt, const int32_t* col, const void* val, in
 int sellb_crs_spmv_host(sellb_crs* m, const void* x_host, void* y_host, int64_t r0, int64_t r1,
                         int32_t accumulate, int32_t unrolled) {
     clear_error();
+    NvtxRange nvtx_("sellb_crs_spmv_host");
     if (!m || !y_host || (!x_host && m->n_cols)) return set_error(SELLB_EPARAM, "NULL argument");
     if (r0 < 0 || r1 > m->n_rows || r0 > r1) return set_error(SELLB_EPARAM, "bad row range");
     if (r0 == r1) return 0;

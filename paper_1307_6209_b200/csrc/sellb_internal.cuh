@@ -13,6 +13,19 @@
 
 #include "../../include/sellb.h"
 
+#include <nvtx3/nvToolsExt.h>
+
+namespace sellb {
+// NVTX range around a host entry point (visible in nsys / ncu timelines;
+// free when no tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace sellb
+
 // ---------------------------------------------------------------------------
 // Device-resident SELL-C-sigma matrix.
 //

@@ -1258,6 +1258,7 @@ extern "C" {
 int sellb_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
                int32_t accumulate, int32_t out_order, void* stream) {
     clear_error();
+    NvtxRange nvtx_("sellb_spmv");
     if (!m || (!x && m->slots) || !y) return set_error(SELLB_EPARAM, "NULL argument");
     DeviceGuard guard(m->device);
     return launch_spmv(m, x, y, c0, c1, accumulate, out_order, (cudaStream_t)stream);
@@ -1484,6 +1485,7 @@ extern "C" {
 int sellb_spmv_host(sellb_mat* m, const void* x_host, void* y_host, int64_t c0, int64_t c1,
                     int32_t accumulate, int32_t out_order, void* stream) {
     clear_error();
+    NvtxRange nvtx_("sellb_spmv_host");
     if (!m || !y_host || (!x_host && m->n_cols)) return set_error(SELLB_EPARAM, "NULL argument");
     if (c0 < 0 || c1 > m->n_chunks || c0 > c1)
         return set_error(SELLB_EPARAM, "chunk range outside the matrix");

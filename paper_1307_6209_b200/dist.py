@@ -389,7 +389,16 @@ class DistSpmv:
             torch.cuda.synchronize(self.device)
             self.graph = None
 
+    def _nvtx(self, name):
+        if self.device.type == "cuda":
+            torch.cuda.nvtx.range_push(name)
+
+    def _nvtx_pop(self):
+        if self.device.type == "cuda":
+            torch.cuda.nvtx.range_pop()
+
     def _step_eager(self):
+        self._nvtx("dist.step")
         if self.x0_recv:
             # the interior chunks may read x_full[0] (padding: 0 * x[0]); it
             # holds +0.0 until the exchange has landed, so a previous step's
@@ -397,7 +406,9 @@ class DistSpmv:
             # 0 * x[0] for the current one
             self.x_full[0:1].zero_()
         works = self._post_exchange()
+        self._nvtx("dist.interior")
         self.engine.run_ranges(self.interior, self.x_full, self.y)
+        self._nvtx_pop()
         for w in works:
             w.wait()
         if self.x0_recv:
@@ -405,9 +416,12 @@ class DistSpmv:
         for p, buf, gidx in self.recv_ops:
             if gidx is not None:
                 self.engine.scatter(buf, gidx, self.x_full)
+        self._nvtx("dist.boundary")
         self.engine.run_ranges(self.boundary, self.x_full, self.y)
+        self._nvtx_pop()
         if self.x0_recv and self.has_padding:
             self.engine.pad_fixup(self.x0_buf, self.y)
+        self._nvtx_pop()
         return self.y
 
 
