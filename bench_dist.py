@@ -47,11 +47,11 @@ def time_parts(ds, device, iters):
 def bench_main(args):
     """Multi-GPU benchmark under torchrun (one process per GPU, NCCL).
 
-    cfg2 (default) -- weak scaling: the 27-point stencil on 128 x 128 x
-    (128 N), one 128^3 z-slab per GPU, halo = one 128x128 plane per
-    neighbour.  cfg5 -- strong scaling: the N = 2^26 banded-random matrix
-    split into N row blocks, each generated and built on its own GPU, halo
-    over the +-2^20 hops."""
+    cfg5 (default, BASELINE configs[4]) -- strong scaling: the N = 2^26
+    banded-random matrix split into N row blocks, each generated and built on
+    its own GPU, halo over the +-65536 / +-2^20 hops.  cfg2 -- weak scaling:
+    the 27-point stencil on 128 x 128 x (128 N), one 128^3 z-slab per GPU,
+    halo = one 128x128 plane per neighbour."""
     import json
     import os
 
@@ -150,11 +150,10 @@ def bench_main(args):
     for _ in range(args.warmup):
         ds.step()
     torch.cuda.synchronize()
-    # one CUDA graph per step (NCCL post included) unless SELLB_DIST_GRAPH=0;
-    # kept only if its replay is bitwise equal to the eager step on all ranks
-    # (tools/dist_graph_selftest.py: NCCL P2P kernels inside the graph)
-    # opt-in (SELLB_DIST_GRAPH=1): a capture with NCCL traffic between two
-    # GPUs has not run yet; eager posting keeps up with cfg5's per-rank SpMV
+    # one CUDA graph per step (NCCL post included), opt-in (SELLB_DIST_GRAPH=1):
+    # a capture with NCCL traffic between two GPUs has not run yet, and eager
+    # posting keeps up with cfg5's per-rank SpMV.  Kept only if its replay
+    # from NaN-poisoned halos equals the eager step bitwise on all ranks.
     graphed = False
     if os.environ.get("SELLB_DIST_GRAPH", "0") == "1":
         graphed = ds.capture()
