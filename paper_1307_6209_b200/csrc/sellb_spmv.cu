@@ -961,9 +961,15 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         const char* e = getenv("SELLB_U");
         return e ? atoi(e) : 0;
     }();
+    // rows of 16..24 entries (the cfg5 banded matrix: 19.7): 8 slots per batch
+    // for the pad-skipping bulk, 6 for the pad-inclusive one (measured on
+    // cfg5, one box: sigma=1 pad-skip U 4 / 6 / 8 -> 728 / 806 / 845 GF/s,
+    // sigma=512 pad-incl 889 / 918 / 908; cfg2 at 26.6 per row keeps U = 8)
+    const bool mid_rows = m->n_rows > 0 && m->nnz >= 16 * m->n_rows &&
+                          m->nnz < 24 * m->n_rows;
     const bool u8 = u_env ? u_env == 8
                           : (sizeof(T) == 4 || m->max_cl > 64 ||
-                             (m->n_rows > 0 && m->nnz >= 24 * m->n_rows));
+                             (m->n_rows > 0 && m->nnz >= 24 * m->n_rows) || (SKIP && mid_rows));
 #define SELLB_LAUNCH(UU, LL, LR, NL, TH, SD)                                                    \
     do {                                                                                        \
         /* LONG instances run next to the row-group kernel: reserve shared */ \
@@ -1086,8 +1092,11 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
         const int32_t* lr = side ? m->long_rest : m->long_rows;
         if (u8) SELLB_LAUNCH(8, true, lr, n_long, m->long_th, side);
         else SELLB_LAUNCH(4, true, lr, n_long, m->long_th, side);
-    } else if (u_env == 6 || (!u_env && m->max_cl > 4 && m->max_cl <= 6 && sizeof(T) == 8)) {
-        // every chunk fits one 6-slot batch (5-point stencils): one round trip
+    } else if (u_env == 6 ||
+               (!u_env && sizeof(T) == 8 && ((m->max_cl > 4 && m->max_cl <= 6) ||
+                                             (!SKIP && !u8 && mid_rows)))) {
+        // every chunk fits one 6-slot batch (5-point stencils): one round
+        // trip; or pad-inclusive rows of 16..24 entries (above)
         SELLB_LAUNCH(6, false, nullptr, 0, 0x7fffffff, false);
     } else {
         if (u8) SELLB_LAUNCH(8, false, nullptr, 0, 0x7fffffff, false);
