@@ -766,7 +766,7 @@ k_spmv_crs_unrolled(const int64_t* __restrict__ rpt, const int32_t* __restrict__
 // (ORD 0) or y[order[p]] (ORD 1), plus the reference's 0 * x[0] term for
 // rows shorter than their chunk (the padding slots it adds).
 template <typename T, bool ACC, bool UNR, int MODE, int ORD, int U, int S>
-__global__ void __launch_bounds__(kThreads, U >= 8 ? 2 : 3)
+__global__ void __launch_bounds__(kThreads, U >= 8 ? 2 : (S * sizeof(T) <= 6144 ? 4 : 3))
 k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
             int64_t r0, int64_t r1, const int32_t* __restrict__ order,
@@ -794,39 +794,41 @@ k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
     bool tail = !UNR;
     for (int64_t wb = base; wb < end; wb += S) {
         const int64_t we = min(wb + (int64_t)S, end);
+        const int wn = (int)(we - wb);                 // window entries (<= S)
+        const T* __restrict__ vw = val + wb;
+        const int32_t* __restrict__ cw = col + wb;
         T v[U];
         int32_t ci[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t t = wb + u * 32 + lane;
+            const int t = u * 32 + lane;
             v[u] = T(0);
             ci[u] = 0;
-            if (t < we) {
-                v[u] = ld_stream(val + t, pol_s);
-                ci[u] = ld_stream(col + t, pol_s);
+            if (t < wn) {
+                v[u] = ld_stream(vw + t, pol_s);
+                ci[u] = ld_stream(cw + t, pol_s);
             }
         }
-        for (int64_t sb = wb; sb < we; sb += B) {
+        for (int sb = 0; sb < wn; sb += B) {
             T xv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                xv[u] = (sb + u * 32 + lane < we) ? ld_x(x + ci[u], pol_x) : T(0);
+                xv[u] = (sb + u * 32 + lane < wn) ? ld_x(x + ci[u], pol_x) : T(0);
             T vn[U];
             int32_t cn[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t t = sb + B + u * 32 + lane;
+                const int t = sb + B + u * 32 + lane;
                 vn[u] = T(0);
                 cn[u] = 0;
-                if (t < we) {
-                    vn[u] = ld_stream(val + t, pol_s);
-                    cn[u] = ld_stream(col + t, pol_s);
+                if (t < wn) {
+                    vn[u] = ld_stream(vw + t, pol_s);
+                    cn[u] = ld_stream(cw + t, pol_s);
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (sb + u * 32 + lane < we)
-                    st[sb - wb + u * 32 + lane] = Arith<T>::mul(v[u], xv[u]);
+                if (sb + u * 32 + lane < wn) st[sb + u * 32 + lane] = Arith<T>::mul(v[u], xv[u]);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 v[u] = vn[u];
@@ -895,14 +897,19 @@ k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
 }
 
 constexpr int kRowsU = 4;
-constexpr int kRowsS = 1024;
+#ifndef SELLB_ROWS_S
+#define SELLB_ROWS_S 768
+#endif
+constexpr int kRowsS = SELLB_ROWS_S;
 
 template <typename T, bool ACC, bool UNR, int MODE, int ORD>
 void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const void* x, void* y,
                  int64_t r0, int64_t r1, const int32_t* order, const int32_t* cl, int64_t n_rows,
                  cudaStream_t st) {
-    // stage of 1024 entries per warp (A/B of 256 / 512 / 1024: cfg2 CRS
-    // 544 / 656 / 697, cfg3 411 / 455 / 455 GF/s)
+    // stage of 768 entries per warp, 4 blocks / SM at 64 registers (A/B of
+    // 256 / 512 / 1024 at 3 blocks: cfg2 CRS 544 / 656 / 697, cfg3 411 / 455 /
+    // 455 GF/s; 768 at 4 blocks vs 1024 at 3: cfg3 447 -> 480, cfg4 288 ->
+    // 323, cfg2 688 -> 656)
     const unsigned grid = (unsigned)grid_for(grid_for(r1 - r0, 32), kThreads / 32);
 #define SELLB_ROWS(UU, SS)                                                                     \
     do {                                                                                       \
