@@ -376,7 +376,10 @@ __global__ void k_side_fill(const int64_t* __restrict__ cs, const int32_t* __res
 
 // Rows longer than the threshold go to the kernel's warp-per-row role.
 // Default threshold 256 slots (SELLB_LONG_TH overrides; <= 0 disables).
-int build_long_rows(sellb_mat* m, cudaStream_t st) {
+// uniform_th > 0: every row longer than uniform_th is long (the packed
+// copy's rule: the row-run kernel walks a row serially, so its longest rows
+// go to the warp-per-row role, which starts first)
+int build_long_rows(sellb_mat* m, cudaStream_t st, int uniform_th = 0) {
     cudaFree(m->long_rows);
     cudaFree(m->chunk_th);
     cudaFree(m->long_groups);
@@ -405,6 +408,7 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     int th = 256, th_hi = 512;      // th_hi 512/1024/2048 on cfg3 sigma=N: 742/674/426
     if (const char* e = getenv("SELLB_LONG_TH")) th = th_hi = atoi(e);
     if (const char* e = getenv("SELLB_LONG_TH_HI")) th_hi = atoi(e);
+    if (uniform_th > 0) th = th_hi = uniform_th;
     // Rule 1: a row is long when it is longer than th_hi, or than
     // max(floor, f * the chunk's k-th longest row) -- i.e. it stands out of
     // its own chunk (unsorted layouts: one or two long rows among short ones,
@@ -416,8 +420,9 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     // 4 C), rule 0 for long scopes whose chunks descend smoothly (measured on
     // cfg3, tools/rule_ab.sh: sigma=1 246 -> 318 GF/s, sigma=128 441 -> 466
     // with rule 1; sigma=512 590 vs 576 keeps rule 0; sigma=N and cfg4 equal).
-    const int rule = getenv("SELLB_LONG_RULE") ? atoi(getenv("SELLB_LONG_RULE"))
-                                               : (m->sigma_eff <= 4 * m->C ? 1 : 0);
+    const int rule = uniform_th > 0 ? 0
+                     : getenv("SELLB_LONG_RULE") ? atoi(getenv("SELLB_LONG_RULE"))
+                                                 : (m->sigma_eff <= 4 * m->C ? 1 : 0);
     const int floor_th = getenv("SELLB_LONG_FLOOR") ? atoi(getenv("SELLB_LONG_FLOOR")) : 48;
     const int kth = std::max(1, getenv("SELLB_LONG_K") ? atoi(getenv("SELLB_LONG_K")) : 8);
     const int fct = std::max(1, getenv("SELLB_LONG_F") ? atoi(getenv("SELLB_LONG_F")) : 2);
@@ -442,7 +447,7 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
                 lo = std::min(lo, h_rl[c * m->C + r]);
                 hi = std::max(hi, h_rl[c * m->C + r]);
             }
-            if ((int64_t)lo * 4 < hi) cth[c] = th;
+            if ((int64_t)lo * 4 < hi || uniform_th > 0) cth[c] = th;
         }
         for (int64_t r = 0; r < m->C; ++r)
             if (h_rl[c * m->C + r] > cth[c]) rows.push_back((int32_t)(c * m->C + r));
@@ -471,7 +476,7 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
     for (int32_t p : rows) long_total += h_rl[p];
     const char* grp_env = getenv("SELLB_LONG_GRP");
     const bool use_groups =
-        m->C % 8 == 0 &&
+        m->C % 8 == 0 && uniform_th <= 0 &&
         (grp_env ? atoi(grp_env) != 0
                  : !(want_side_all && long_total * 4 <= std::max<int64_t>(m->nnz, 1)));
     if (use_groups) {
@@ -557,9 +562,16 @@ int build_long_rows(sellb_mat* m, cudaStream_t st) {
 // at prpt[p] .. prpt[p+1] (prpt = exclusive scan of row_lengths) -- the
 // SELL layout without its padding, read by the row-run kernel.
 // ---------------------------------------------------------------------------
-__global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+// a stored row's entries in the packed copy: its length, or 0 for a row the
+// warp-per-row role sums (chunk wider than long_th, row longer than chunk_th)
+__global__ void k_packed_len(const int32_t* __restrict__ rl, const int32_t* __restrict__ cl,
+                             const int32_t* __restrict__ chunk_th, int long_th, int64_t n,
+                             int64_t C, int64_t* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = in[i];
+    if (i >= n) return;
+    const int64_t c = i / C;
+    const int len = rl[i];
+    out[i] = (chunk_th && cl[c] > long_th && len > chunk_th[c]) ? 0 : len;
 }
 
 template <typename T>
@@ -573,7 +585,7 @@ __global__ void k_packed_fill(const int64_t* __restrict__ cs, const int32_t* __r
     const int64_t chunk = p / C;
     const int64_t src = cs[chunk] + (p - chunk * C);
     const int64_t dst = prpt[p];
-    const int len = rl[p];
+    const int len = (int)(prpt[p + 1] - dst);        // 0 for the warp-per-row role's rows
     for (int j = lane; j < len; j += 32) {
         pcol[dst + j] = col[src + (int64_t)j * C];
         pval[dst + j] = val[src + (int64_t)j * C];
@@ -599,7 +611,11 @@ namespace sellb {
 // sigma=1 324 -> 450 GF/s; sigma=128 / 512 and cfg4 are faster in the SELL
 // bulk role, and the model leaves them there)
 int build_packed(sellb_mat* m, cudaStream_t st, int force) {
+    const bool had = m->pcol != nullptr;
     free_packed(m);
+    if (had) {   // the SELL kernels' own long-row rule again
+        if (int rc = build_long_rows(m, st)) return rc;
+    }
     bool from_env = false;
     if (force == -2) {
         const char* e = getenv("SELLB_PACKED");
@@ -643,13 +659,19 @@ int build_packed(sellb_mat* m, cudaStream_t st, int force) {
             return 0;
         }
     }
+    // the packed copy's long rows: rows longer than kPackedLong go to the
+    // warp-per-row role (side table), started first on a side stream; the
+    // packed copy leaves them out
+    int plong = kPackedLong;
+    if (const char* e = getenv("SELLB_PACKED_LONG")) plong = std::max(1, atoi(e));
+    if (int rc = build_long_rows(m, st, plong)) return rc;
     if (int rc = alloc_dev((void**)&m->prpt, (m->n_pad + 1) * 8)) return rc;
     {
         DBuf d_len;
         SELLB_CU(d_len.alloc((m->n_pad + 1) * 8, st));
         SELLB_CU(cudaMemsetAsync(d_len.p, 0, 8, st));
-        k_widen<<<(unsigned)grid_for(m->n_pad, 256), 256, 0, st>>>(m->rl, m->n_pad,
-                                                                    d_len.as<int64_t>() + 1);
+        k_packed_len<<<(unsigned)grid_for(m->n_pad, 256), 256, 0, st>>>(
+            m->rl, m->cl, m->chunk_th, m->long_th, m->n_pad, m->C, d_len.as<int64_t>() + 1);
         size_t tmp_bytes = 0;
         SELLB_CU(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_len.as<int64_t>(), m->prpt,
                                                m->n_pad + 1, st));
@@ -658,8 +680,11 @@ int build_packed(sellb_mat* m, cudaStream_t st, int force) {
         SELLB_CU(cub::DeviceScan::InclusiveSum(d_tmp.p, tmp_bytes, d_len.as<int64_t>(), m->prpt,
                                                m->n_pad + 1, st));
     }
-    if (int rc = alloc_dev((void**)&m->pcol, std::max<int64_t>(total, 1) * 4)) return rc;
-    if (int rc = alloc_dev(&m->pval, std::max<int64_t>(total, 1) * vs)) return rc;
+    int64_t packed_total = 0;
+    SELLB_CU(cudaMemcpyAsync(&packed_total, m->prpt + m->n_pad, 8, cudaMemcpyDeviceToHost, st));
+    SELLB_CU(cudaStreamSynchronize(st));
+    if (int rc = alloc_dev((void**)&m->pcol, std::max<int64_t>(packed_total, 1) * 4)) return rc;
+    if (int rc = alloc_dev(&m->pval, std::max<int64_t>(packed_total, 1) * vs)) return rc;
     const unsigned grid = (unsigned)grid_for(m->n_pad * 32, 256);
     if (m->dtype == SELLB_F32)
         k_packed_fill<float><<<grid, 256, 0, st>>>(m->cs, m->rl, m->col, (const float*)m->val,
@@ -671,7 +696,7 @@ int build_packed(sellb_mat* m, cudaStream_t st, int force) {
                                                    (double*)m->pval);
     if (int rc = check_stream_error()) return rc;
     SELLB_CU(cudaStreamSynchronize(st));
-    m->n_packed = total;
+    m->n_packed = packed_total;
     return 0;
 }
 

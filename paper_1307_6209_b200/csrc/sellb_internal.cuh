@@ -172,6 +172,8 @@ bool is_pinned(const void* p);
 int ensure_host_mirror(void** slot, size_t bytes);
 
 int build_packed(sellb_mat* m, cudaStream_t st, int force);
+constexpr int kPackedLong = 128;      // packed copy: longer rows -> warp-per-row role
+                                      // (cfg3 sigma=1, threshold 64 / 128 / 256 / 512: 515 / 539 / 512 / 486 GF/s)
 
 inline int64_t grid_for(int64_t n, int threads) { return (n + threads - 1) / threads; }
 

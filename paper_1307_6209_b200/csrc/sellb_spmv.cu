@@ -770,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, U >= 8 ? 2 : (S * sizeof(T) <= 6144 
 k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
             int64_t r0, int64_t r1, const int32_t* __restrict__ order,
-            const int32_t* __restrict__ cl, int64_t n_rows) {
+            const int32_t* __restrict__ cl, const int32_t* __restrict__ rl, int64_t n_rows) {
     constexpr int WPB = kThreads / 32;
     constexpr int B = 32 * U;
     static_assert(S % B == 0, "stage must hold whole sub-batches");
@@ -891,7 +891,9 @@ k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
             y[i] = sum;
         }
     } else {
-        if ((int64_t)(e - s) < (int64_t)cl[i >> 5]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+        const int len = rl[i];
+        if ((int64_t)(e - s) != len) return;          // a long row: the warp-per-row role's
+        if (len < cl[i >> 5]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
         store_row<T, ACC, ORD>(y, order, i, n_rows, sum);
     }
 }
@@ -904,8 +906,8 @@ constexpr int kRowsS = SELLB_ROWS_S;
 
 template <typename T, bool ACC, bool UNR, int MODE, int ORD>
 void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const void* x, void* y,
-                 int64_t r0, int64_t r1, const int32_t* order, const int32_t* cl, int64_t n_rows,
-                 cudaStream_t st) {
+                 int64_t r0, int64_t r1, const int32_t* order, const int32_t* cl,
+                 const int32_t* rl, int64_t n_rows, cudaStream_t st) {
     // stage of 768 entries per warp, 4 blocks / SM at 64 registers (A/B of
     // 256 / 512 / 1024 at 3 blocks: cfg2 CRS 544 / 656 / 697, cfg3 411 / 455 /
     // 455 GF/s; 768 at 4 blocks vs 1024 at 3: cfg3 447 -> 480, cfg4 288 ->
@@ -923,13 +925,83 @@ void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const 
             attr_ |= 1u << (dev_ & 31);                                                        \
         }                                                                                      \
         kern<<<grid, kThreads, smem_, st>>>(rpt, col, (const T*)val, (const T*)x, (T*)y, r0,   \
-                                            r1, order, cl, n_rows);                            \
+                                            r1, order, cl, rl, n_rows);                        \
     } while (0)
     // U = 4 (B = 128-entry sub-batches, 3 blocks / SM): U = 8 measured slower
     // everywhere (cfg2 / cfg3 / cfg4 CRS 698 / 452 / 289 -> 622 / 380 / 239)
     SELLB_ROWS(kRowsU, kRowsS);
 #undef SELLB_ROWS
     count_launches();
+}
+
+// The warp-per-row role alone (one warp per row of rows[], side table or
+// SELL arrays): the long rows next to the packed copy's row-run kernel.
+template <typename T, bool ACC, int ORD>
+__global__ void __launch_bounds__(kThreads)
+k_long_rows(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+            const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
+            const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
+            const int32_t* __restrict__ order, int64_t C, int64_t p0, int64_t p1, int64_t n_rows,
+            const int32_t* __restrict__ rows, int64_t n_long, int l2pol,
+            const int64_t* __restrict__ side_off, const int32_t* __restrict__ side_col,
+            const T* __restrict__ side_val) {
+    constexpr int WPB = kThreads / 32;
+    __shared__ T stage[WPB][kSeg * 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t k = (int64_t)blockIdx.x * WPB + warp;
+    if (k >= n_long) return;
+    const int64_t p = rows[k];
+    if (p < p0 || p >= p1) return;
+    const uint64_t pol_s = make_policy(l2pol & 0xf);
+    const uint64_t pol_x = make_policy((l2pol >> 4) & 0xf);
+    const int64_t chunk = p / C;
+    if (side_off) {
+        const int64_t o = side_off[k];
+        long_row_at<T, ACC, ORD>(side_val + o, side_col + o, 1, rl[p], cl[chunk], x, y, order, p,
+                                 n_rows, lane, pol_s, pol_x, stage[warp]);
+    } else {
+        const int64_t base = cs[chunk] + (p - chunk * C);
+        long_row_at<T, ACC, ORD>(val + base, col + base, C, rl[p], cl[chunk], x, y, order, p,
+                                 n_rows, lane, pol_s, pol_x, stage[warp]);
+    }
+}
+
+// The packed copy: its long rows (rows longer than kPackedLong) by the
+// warp-per-row role on the highest-priority side stream, started first; the
+// row-run kernel (MODE 1) on the caller's stream; joined.
+template <typename T, bool ACC, int ORD>
+int launch_packed(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1,
+                  cudaStream_t st) {
+    const int64_t n_long = m->long_rows ? m->n_long : 0;
+    sellb_mat* mm = const_cast<sellb_mat*>(m);
+    std::unique_lock<std::mutex> lk(mm->long_mu, std::defer_lock);
+    if (n_long) {
+        lk.lock();
+        if (!mm->long_ready) {
+            int prio_lo = 0, prio_hi = 0;
+            SELLB_CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+            SELLB_CU(cudaStreamCreateWithPriority(&mm->s_long, cudaStreamNonBlocking, prio_hi));
+            SELLB_CU(cudaEventCreateWithFlags(&mm->ev_fork, cudaEventDisableTiming));
+            SELLB_CU(cudaEventCreateWithFlags(&mm->ev_join, cudaEventDisableTiming));
+            mm->long_ready = true;
+        }
+        SELLB_CU(cudaEventRecord(mm->ev_fork, st));
+        SELLB_CU(cudaStreamWaitEvent(mm->s_long, mm->ev_fork, 0));
+        const bool side = m->side_off && m->n_rest == n_long;
+        const int l2pol = (int64_t)m->n_cols * (int64_t)sizeof(T) > (64LL << 20) ? 0x21 : 0x20;
+        k_long_rows<T, ACC, ORD><<<(unsigned)grid_for(n_long, kThreads / 32), kThreads, 0,
+                                   mm->s_long>>>(
+            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order, m->C,
+            p0, p1, m->n_rows, side ? m->long_rest : m->long_rows, n_long, l2pol,
+            side ? m->side_off : nullptr, side ? m->side_col : nullptr,
+            (const T*)(side ? m->side_val : nullptr));
+        count_launches();
+        SELLB_CU(cudaEventRecord(mm->ev_join, mm->s_long));
+    }
+    launch_rows<T, ACC, false, 1, ORD>(m->prpt, m->pcol, m->pval, x, y, p0, p1, m->order, m->cl,
+                                       m->rl, m->n_rows, st);
+    if (n_long) SELLB_CU(cudaStreamWaitEvent(st, mm->ev_join, 0));
+    return 0;
 }
 
 template <typename T, int CC, bool SKIP, bool ACC, int ORD>
@@ -1130,18 +1202,10 @@ int dispatch_sell(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_
     const bool skip = m->variant == SELLB_VARIANT_PAD_SKIP && m->rl;
     if (skip && m->pcol && m->C == 32) {
         // the packed stored-order copy through the row-run kernel (MODE 1)
-        if (acc) {
-            if (ord) launch_rows<T, true, false, 1, 1>(m->prpt, m->pcol, m->pval, x, y, p0, p1,
-                                                       m->order, m->cl, m->n_rows, st);
-            else launch_rows<T, true, false, 1, 0>(m->prpt, m->pcol, m->pval, x, y, p0, p1,
-                                                   m->order, m->cl, m->n_rows, st);
-        } else {
-            if (ord) launch_rows<T, false, false, 1, 1>(m->prpt, m->pcol, m->pval, x, y, p0, p1,
-                                                        m->order, m->cl, m->n_rows, st);
-            else launch_rows<T, false, false, 1, 0>(m->prpt, m->pcol, m->pval, x, y, p0, p1,
-                                                    m->order, m->cl, m->n_rows, st);
-        }
-        return 0;
+        if (acc) return ord ? launch_packed<T, true, 1>(m, x, y, p0, p1, st)
+                            : launch_packed<T, true, 0>(m, x, y, p0, p1, st);
+        return ord ? launch_packed<T, false, 1>(m, x, y, p0, p1, st)
+                   : launch_packed<T, false, 0>(m, x, y, p0, p1, st);
     }
     if (m->C == 32) {
         return skip ? dispatch_acc<T, 32, true>(m, x, y, p0, p1, acc, ord, st)
@@ -1233,7 +1297,7 @@ int launch_spmv_crs(const int64_t* rpt, const int32_t* col, const void* val, int
     static const bool scalar = getenv("SELLB_CRS_SCALAR") && atoi(getenv("SELLB_CRS_SCALAR"));
     if (!scalar) {
 #define SELLB_CRST(T, A, UN)                                                                  \
-    launch_rows<T, A, UN, 0, 0>(rpt, col, val, x, y, r0, r1, nullptr, nullptr, 0, st)
+    launch_rows<T, A, UN, 0, 0>(rpt, col, val, x, y, r0, r1, nullptr, nullptr, nullptr, 0, st)
         if (dtype == SELLB_F32) {
             if (unrolled) { if (accumulate) SELLB_CRST(float, true, true); else SELLB_CRST(float, false, true); }
             else { if (accumulate) SELLB_CRST(float, true, false); else SELLB_CRST(float, false, false); }
