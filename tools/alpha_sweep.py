@@ -91,7 +91,32 @@ def report(layouts_json, ncu_csv, times_json):
         per.setdefault(r["ID"], {})[r["Metric Name"]] = (float(r["Metric Value"]),
                                                          r["Metric Unit"])
     ids = sorted(per, key=int)
-    assert len(ids) == len(rows), (len(ids), len(rows))
+    # one SpMV may be two launches (the packed copy's row-run kernel plus the
+    # warp-per-row kernel for its long rows): sum the DRAM bytes of each
+    # layout's launches
+    def n_launch(row):
+        packed = "+packed" in row["variant"]
+        return 2 if packed and row["long_rows"]["n_long"] > 0 else 1
+    groups, k = [], 0
+    for row in rows:
+        n = n_launch(row)
+        groups.append(ids[k:k + n])
+        k += n
+    assert k == len(ids), (k, len(ids))
+    merged = {}
+    for g in groups:
+        acc = {}
+        for i in g:
+            for name, (v, u) in per[i].items():
+                f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u)
+                if f is None:
+                    acc.setdefault(name, (v, u))
+                    continue
+                prev = acc.get(name, (0.0, "byte"))[0]
+                acc[name] = (prev + v * f, "byte")
+        merged[g[0]] = acc
+    per = merged
+    ids = [g[0] for g in groups]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(
         os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
