@@ -1412,9 +1412,9 @@ __global__ void k_chunk_maxcol(const int64_t* __restrict__ cs, const int32_t* __
 // landed).
 int pipe_setup(sellb_mat* m) {
     if (m->pipe_ready) return 0;
-    // cfg5 (tools/pcie_probe.py box): depth 4 / 8 -> pinned 14.4 / 13.4 ms, pageable
-    // staged 28.0 / 25.9 ms per step; cfg2 (tools/e2e_probe.py) is flat from 4 up
-    int want = 8;
+    // cfg5: depth 4 / 8 / 16 -> pinned 13.9 / 13.0 / 12.6 ms per step (y by DMA),
+    // pageable staged 28.0 / 25.9 ms (depth 4 / 8); cfg2 is flat from 4 up
+    int want = 16;
     if (const char* e = getenv("SELLB_PIPE")) want = std::max(1, std::min(atoi(e), sellb_mat::kPipe));
     const int P = (int)std::min<int64_t>(want, std::max<int64_t>(m->n_chunks, 1));
     std::vector<int32_t> maxcol(std::max<int64_t>(m->n_chunks, 1), 0);
@@ -1475,7 +1475,12 @@ int spmv_host_pipelined(sellb_mat* m, const void* x_host, void* y_host, cudaStre
     const int P = m->n_pieces;
     const bool x_pinned = is_pinned(x_host);
     const bool y_pinned = is_pinned(y_host);
-    const bool zero_copy = !getenv("SELLB_NO_ZEROCOPY");
+    // y of a pinned caller buffer goes back by DMA per row block (cfg5, depth
+    // 16: 12.6 ms vs 13.2 ms with the kernels storing over PCIe); a pageable
+    // y is stored by the kernels straight into the mapped mirror (one PCIe
+    // crossing, no pageable D2H copy: 27 ms vs 128 ms per step)
+    static const bool no_zc = getenv("SELLB_NO_ZEROCOPY") != nullptr;
+    const bool zero_copy = !no_zc && !y_pinned;
     if (!x_pinned) {
         if (int rc = ensure_host_mirror(&m->hx, (size_t)m->n_cols * vs)) return rc;
     }
