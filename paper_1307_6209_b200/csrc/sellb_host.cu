@@ -8,7 +8,8 @@
 // only ~4 GB/s and all 16 together ~53 GB/s.  So the library stages pageable
 // vectors itself: a pool of host threads copies each x piece into a pinned
 // mirror while the previous piece is on the wire, and copies each finished
-// row block of y out of a pinned (mapped) mirror while later blocks compute.
+// row block of y out of a pinned (mapped) mirror the kernels store into
+// while later blocks compute.  Pinned caller vectors need none of this.
 #include <algorithm>
 #include <condition_variable>
 #include <cstring>
