@@ -267,13 +267,16 @@ __device__ __forceinline__ void long_row_at(const T* __restrict__ vp,
                                             uint64_t pol_x, T* __restrict__ stage) {
     const int64_t C = stride;
     T sum = T(0);
-    for (int j0 = 0; j0 < len; j0 += 32 * kSeg) {
-        T prod[kSeg];
-        int32_t c[kSeg];
+    // batch b's products are staged and added while batch b+1's val / col
+    // loads and x gathers are already in flight (one round trip per batch
+    // hidden behind the 128-step add chain)
+    T prod[kSeg];
+    {
         T v[kSeg];
+        int32_t c[kSeg];
 #pragma unroll
         for (int s = 0; s < kSeg; ++s) {
-            const int j = j0 + s * 32 + lane;
+            const int j = s * 32 + lane;
             v[s] = T(0);
             c[s] = 0;
             if (j < len) {
@@ -282,24 +285,44 @@ __device__ __forceinline__ void long_row_at(const T* __restrict__ vp,
             }
         }
 #pragma unroll
+        for (int s = 0; s < kSeg; ++s)
+            prod[s] = (s * 32 + lane < len) ? Arith<T>::mul(v[s], ld_x(x + c[s], pol_x)) : T(0);
+    }
+    for (int j0 = 0; j0 < len; j0 += 32 * kSeg) {
+        const int jn = j0 + 32 * kSeg;
+        T vn[kSeg];
+        int32_t cn[kSeg];
+#pragma unroll
         for (int s = 0; s < kSeg; ++s) {
-            const int j = j0 + s * 32 + lane;
-            prod[s] = (j < len) ? Arith<T>::mul(v[s], ld_x(x + c[s], pol_x)) : T(0);
+            const int j = jn + s * 32 + lane;
+            vn[s] = T(0);
+            cn[s] = 0;
+            if (j < len) {
+                vn[s] = ld_stream(vp + (int64_t)j * C, pol_s);
+                cn[s] = ld_stream(cp + (int64_t)j * C, pol_s);
+            }
         }
         __syncwarp();                        // previous batch fully consumed
 #pragma unroll
         for (int s = 0; s < kSeg; ++s) stage[s * 32 + lane] = prod[s];
         __syncwarp();
+        T xn[kSeg];
+#pragma unroll
+        for (int s = 0; s < kSeg; ++s)
+            xn[s] = (jn + s * 32 + lane < len) ? ld_x(x + cn[s], pol_x) : T(0);
         const int nb = min(len - j0, kSeg * 32);      // warp-uniform
         int i = 0;
-        for (; i + 16 <= nb; i += 16) {
-            T q[16];
+        for (; i + 8 <= nb; i += 8) {
+            T q[8];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) q[k] = stage[i + k];
+            for (int k = 0; k < 8; ++k) q[k] = stage[i + k];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) sum = Arith<T>::add(sum, q[k]);
+            for (int k = 0; k < 8; ++k) sum = Arith<T>::add(sum, q[k]);
         }
         for (; i < nb; ++i) sum = Arith<T>::add(sum, stage[i]);
+#pragma unroll
+        for (int s = 0; s < kSeg; ++s)
+            prod[s] = (jn + s * 32 + lane < len) ? Arith<T>::mul(vn[s], xn[s]) : T(0);
     }
     if (len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
     if (lane == 0) store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
