@@ -75,7 +75,10 @@ def bench_main(args):
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    tdist.init_process_group("nccl", device_id=device)
+    import datetime
+    # a wedged peer fails the run within minutes instead of NCCL's default 10
+    tdist.init_process_group("nccl", device_id=device,
+                             timeout=datetime.timedelta(seconds=300))
     C, sigma = args.C, args.sigma
     dt_np = np.float32 if args.dtype == "f32" else np.float64
     s_v = 4 if args.dtype == "f32" else 8
