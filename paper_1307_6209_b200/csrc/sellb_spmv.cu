@@ -550,9 +550,12 @@ template <typename T, int CC, bool SKIP, bool ACC, int ORD, int U, bool LONG>
 #ifndef SELLB_F32_BLOCKS
 #define SELLB_F32_BLOCKS 6   // fp32 U=8: 40 regs, 48 warps/SM (tools/f32occ_ab.sh: cfg4 f32 881 -> 1050)
 #endif
+// U = 6: 8 blocks (32 registers) for the plain C = 32 pad-inclusive store
+// (no spills; cfg5 919 -> 926 GF/s), 6 for the instances that would spill
 __global__ void __launch_bounds__(kThreads, U == 4 ? (LONG ? 6 : 8)
-                                             : (U == 6 ? 6 : (sizeof(T) == 4 ? SELLB_F32_BLOCKS
-                                                                            : SELLB_F64_BLOCKS)))
+                                             : (U == 6 ? ((CC == 32 && !SKIP && !ACC) ? 8 : 6)
+                                                       : (sizeof(T) == 4 ? SELLB_F32_BLOCKS
+                                                                         : SELLB_F64_BLOCKS)))
 k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
             const int32_t* __restrict__ rl, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
