@@ -792,7 +792,7 @@ k_spmv_crs_unrolled(const int64_t* __restrict__ rpt, const int32_t* __restrict__
 // (ORD 0) or y[order[p]] (ORD 1), plus the reference's 0 * x[0] term for
 // rows shorter than their chunk (the padding slots it adds).
 template <typename T, bool ACC, bool UNR, int MODE, int ORD, int U, int S>
-__global__ void __launch_bounds__(kThreads, U >= 8 ? 2 : (S * sizeof(T) <= 6144 ? 4 : 3))
+__global__ void __launch_bounds__(kThreads, U >= 8 ? 2 : (S * sizeof(T) <= 6144 && !(MODE == 0 && sizeof(T) == 8 && (ACC || UNR)) ? 4 : 3))
 k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
             const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y,
             int64_t r0, int64_t r1, const int32_t* __restrict__ order,
@@ -803,124 +803,155 @@ k_spmv_rows(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
     extern __shared__ __align__(16) uint8_t rows_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     T* st = reinterpret_cast<T*>(rows_smem) + (size_t)warp * S;
-    const int64_t rb = r0 + ((int64_t)blockIdx.x * WPB + warp) * 32;
-    if (rb >= r1) return;
-    const int64_t i = rb + lane;
-    const bool valid = i < r1;
-    const int64_t last = min(rb + 32, r1);
-    const int64_t s = valid ? rpt[i] : 0;
-    const int64_t e = valid ? rpt[i + 1] : 0;
-    const int64_t base = rpt[rb];
-    const int64_t end = rpt[last];
     const uint64_t pol_s = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
-    const int64_t m4 = s + ((e - s) & ~(int64_t)3);
-    int64_t pos = s;
-    T sum = T(0), t0 = T(0), t1 = T(0), t2 = T(0), t3 = T(0);
-    bool tail = !UNR;
-    for (int64_t wb = base; wb < end; wb += S) {
-        const int64_t we = min(wb + (int64_t)S, end);
-        const int wn = (int)(we - wb);                 // window entries (<= S)
-        const T* __restrict__ vw = val + wb;
-        const int32_t* __restrict__ cw = col + wb;
-        T v[U];
-        int32_t ci[U];
+    // persistent warps: group g = 32 rows; the first sub-batch of the next
+    // group (and its offsets) is fetched before this group's in-order walks,
+    // so the matrix stream stays in flight while a warp adds
+    const int64_t n_groups = (r1 - r0 + 31) / 32;
+    const int64_t GW = (int64_t)gridDim.x * WPB;
+    int64_t g = (int64_t)blockIdx.x * WPB + warp;
+    if (g >= n_groups) return;
+    auto group_base = [&](int64_t gg) { return rpt[r0 + gg * 32]; };
+    auto group_end = [&](int64_t gg) { return rpt[min(r0 + gg * 32 + 32, r1)]; };
+    T v[U];
+    int32_t ci[U];
+    auto load_first = [&](int64_t b0, int64_t en) {
+        const int64_t wn0 = min((int64_t)S, en - b0);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = u * 32 + lane;
             v[u] = T(0);
             ci[u] = 0;
-            if (t < wn) {
-                v[u] = ld_stream(vw + t, pol_s);
-                ci[u] = ld_stream(cw + t, pol_s);
+            if (t < wn0) {
+                v[u] = ld_stream(val + b0 + t, pol_s);
+                ci[u] = ld_stream(col + b0 + t, pol_s);
             }
         }
-        for (int sb = 0; sb < wn; sb += B) {
-            T xv[U];
+    };
+    int64_t base = group_base(g), end = group_end(g);
+    load_first(base, end);
+    while (true) {
+        const int64_t rb = r0 + g * 32;
+        const int64_t i = rb + lane;
+        const bool valid = i < r1;
+        const int64_t s = valid ? rpt[i] : 0;
+        const int64_t e = valid ? rpt[i + 1] : 0;
+        const int64_t gn = g + GW;
+        const bool has_next = gn < n_groups;
+        const int64_t nbase = has_next ? group_base(gn) : 0;
+        const int64_t nend = has_next ? group_end(gn) : 0;
+        const int64_t m4 = s + ((e - s) & ~(int64_t)3);
+        int64_t pos = s;
+        T sum = T(0), t0 = T(0), t1 = T(0), t2 = T(0), t3 = T(0);
+        bool tail = !UNR;
+        bool prefetched = false;
+        for (int64_t wb = base; wb < end; wb += S) {
+            const int64_t we = min(wb + (int64_t)S, end);
+            const int wn = (int)(we - wb);             // window entries (<= S)
+            const T* __restrict__ vw = val + wb;
+            const int32_t* __restrict__ cw = col + wb;
+            if (wb != base) load_first(wb, end);
+            for (int sb = 0; sb < wn; sb += B) {
+                T xv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                xv[u] = (sb + u * 32 + lane < wn) ? ld_x(x + ci[u], pol_x) : T(0);
-            T vn[U];
-            int32_t cn[U];
+                for (int u = 0; u < U; ++u)
+                    xv[u] = (sb + u * 32 + lane < wn) ? ld_x(x + ci[u], pol_x) : T(0);
+                T vn[U];
+                int32_t cn[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int t = sb + B + u * 32 + lane;
-                vn[u] = T(0);
-                cn[u] = 0;
-                if (t < wn) {
-                    vn[u] = ld_stream(vw + t, pol_s);
-                    cn[u] = ld_stream(cw + t, pol_s);
+                for (int u = 0; u < U; ++u) {
+                    const int t = sb + B + u * 32 + lane;
+                    vn[u] = T(0);
+                    cn[u] = 0;
+                    if (t < wn) {
+                        vn[u] = ld_stream(vw + t, pol_s);
+                        cn[u] = ld_stream(cw + t, pol_s);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (sb + u * 32 + lane < wn)
+                        st[sb + u * 32 + lane] = Arith<T>::mul(v[u], xv[u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    v[u] = vn[u];
+                    ci[u] = cn[u];
                 }
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (sb + u * 32 + lane < wn) st[sb + u * 32 + lane] = Arith<T>::mul(v[u], xv[u]);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                v[u] = vn[u];
-                ci[u] = cn[u];
+            if (we == end && has_next) {               // the next group's stream
+                load_first(nbase, nend);
+                prefetched = true;
             }
+            __syncwarp();
+            // phase 2: this row's products inside the window, in order
+            const T* sp = st - wb;
+            if (!UNR) {
+                const int64_t stop = min(e, we);
+                for (; pos + 4 <= stop; pos += 4) {
+                    const T a0 = sp[pos], a1 = sp[pos + 1], a2 = sp[pos + 2], a3 = sp[pos + 3];
+                    sum = Arith<T>::add(sum, a0);
+                    sum = Arith<T>::add(sum, a1);
+                    sum = Arith<T>::add(sum, a2);
+                    sum = Arith<T>::add(sum, a3);
+                }
+                for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
+            } else {
+                const int64_t stop4 = min(m4, we);
+                // whole groups of four (pos - s is a multiple of 4 here unless a
+                // window boundary split a group: then one entry at a time)
+                while (pos < stop4) {
+                    if (((pos - s) & 3) == 0 && pos + 4 <= stop4) {
+                        t0 = Arith<T>::add(t0, sp[pos]);
+                        t1 = Arith<T>::add(t1, sp[pos + 1]);
+                        t2 = Arith<T>::add(t2, sp[pos + 2]);
+                        t3 = Arith<T>::add(t3, sp[pos + 3]);
+                        pos += 4;
+                    } else {
+                        const int k = (int)((pos - s) & 3);
+                        const T pr = sp[pos];
+                        if (k == 0) t0 = Arith<T>::add(t0, pr);
+                        else if (k == 1) t1 = Arith<T>::add(t1, pr);
+                        else if (k == 2) t2 = Arith<T>::add(t2, pr);
+                        else t3 = Arith<T>::add(t3, pr);
+                        ++pos;
+                    }
+                }
+                const int64_t stop = min(e, we);
+                if (pos >= m4 && pos < stop && !tail) {
+                    const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
+                    sum = ACC ? Arith<T>::add(y[i], comb) : comb;
+                    tail = true;
+                }
+                for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
+            }
+            __syncwarp();
         }
-        __syncwarp();
-        // phase 2: this row's products inside the window, in order
-        const T* sp = st - wb;
-        if (!UNR) {
-            const int64_t stop = min(e, we);
-            for (; pos + 4 <= stop; pos += 4) {
-                const T a0 = sp[pos], a1 = sp[pos + 1], a2 = sp[pos + 2], a3 = sp[pos + 3];
-                sum = Arith<T>::add(sum, a0);
-                sum = Arith<T>::add(sum, a1);
-                sum = Arith<T>::add(sum, a2);
-                sum = Arith<T>::add(sum, a3);
-            }
-            for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
-        } else {
-            const int64_t stop4 = min(m4, we);
-            // whole groups of four (pos - s is a multiple of 4 here unless a
-            // window boundary split a group: then one entry at a time)
-            while (pos < stop4) {
-                if (((pos - s) & 3) == 0 && pos + 4 <= stop4) {
-                    t0 = Arith<T>::add(t0, sp[pos]);
-                    t1 = Arith<T>::add(t1, sp[pos + 1]);
-                    t2 = Arith<T>::add(t2, sp[pos + 2]);
-                    t3 = Arith<T>::add(t3, sp[pos + 3]);
-                    pos += 4;
+        if (!prefetched && has_next) load_first(nbase, nend);   // an empty group
+        if (valid) {
+            if (MODE == 0) {
+                if (!UNR) {
+                    y[i] = ACC ? Arith<T>::add(y[i], sum) : sum;
                 } else {
-                    const int k = (int)((pos - s) & 3);
-                    const T pr = sp[pos];
-                    if (k == 0) t0 = Arith<T>::add(t0, pr);
-                    else if (k == 1) t1 = Arith<T>::add(t1, pr);
-                    else if (k == 2) t2 = Arith<T>::add(t2, pr);
-                    else t3 = Arith<T>::add(t3, pr);
-                    ++pos;
+                    if (!tail) {
+                        const T comb =
+                            Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
+                        sum = ACC ? Arith<T>::add(y[i], comb) : comb;
+                    }
+                    y[i] = sum;
+                }
+            } else {
+                const int len = rl[i];
+                if ((int64_t)(e - s) == len) {        // else a long row: the warp-per-row role's
+                    if (len < cl[i >> 5]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+                    store_row<T, ACC, ORD>(y, order, i, n_rows, sum);
                 }
             }
-            const int64_t stop = min(e, we);
-            if (pos >= m4 && pos < stop && !tail) {
-                const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
-                sum = ACC ? Arith<T>::add(y[i], comb) : comb;
-                tail = true;
-            }
-            for (; pos < stop; ++pos) sum = Arith<T>::add(sum, sp[pos]);
         }
-        __syncwarp();
-    }
-    if (!valid) return;
-    if (MODE == 0) {
-        if (!UNR) {
-            y[i] = ACC ? Arith<T>::add(y[i], sum) : sum;
-        } else {
-            if (!tail) {
-                const T comb = Arith<T>::add(Arith<T>::add(Arith<T>::add(t0, t1), t2), t3);
-                sum = ACC ? Arith<T>::add(y[i], comb) : comb;
-            }
-            y[i] = sum;
-        }
-    } else {
-        const int len = rl[i];
-        if ((int64_t)(e - s) != len) return;          // a long row: the warp-per-row role's
-        if (len < cl[i >> 5]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
-        store_row<T, ACC, ORD>(y, order, i, n_rows, sum);
+        if (!has_next) break;
+        g = gn;
+        base = nbase;
+        end = nend;
     }
 }
 
@@ -938,18 +969,32 @@ void launch_rows(const int64_t* rpt, const int32_t* col, const void* val, const 
     // 256 / 512 / 1024 at 3 blocks: cfg2 CRS 544 / 656 / 697, cfg3 411 / 455 /
     // 455 GF/s; 768 at 4 blocks vs 1024 at 3: cfg3 447 -> 480, cfg4 288 ->
     // 323, cfg2 688 -> 656)
-    const unsigned grid = (unsigned)grid_for(grid_for(r1 - r0, 32), kThreads / 32);
+    // persistent grid: one wave (the kernel's resident blocks per SM x SMs),
+    // each warp walks groups warp, warp + all warps, ...
+    static const int sms_ = [] {
+        int d = 0, n = 148;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+        return n;
+    }();
+    const int64_t groups_ = grid_for(grid_for(r1 - r0, 32), kThreads / 32);
 #define SELLB_ROWS(UU, SS)                                                                     \
     do {                                                                                       \
         auto kern = k_spmv_rows<T, ACC, UNR, MODE, ORD, UU, SS>;                               \
         constexpr size_t smem_ = (size_t)(kThreads / 32) * SS * sizeof(T);                     \
         static unsigned attr_ = 0;                                                             \
+        static int bps_ = 0;                                                                   \
         int dev_ = 0;                                                                          \
         cudaGetDevice(&dev_);                                                                  \
         if (!(attr_ & (1u << (dev_ & 31)))) {                                                  \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_); \
             attr_ |= 1u << (dev_ & 31);                                                        \
+            if (!bps_ && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_, kern, kThreads,  \
+                                                                       smem_) != cudaSuccess) \
+                bps_ = 1;                                                                      \
         }                                                                                      \
+        const unsigned grid = (unsigned)std::max<int64_t>(                                     \
+            1, std::min<int64_t>(groups_, (int64_t)sms_ * std::max(bps_, 1)));                 \
         kern<<<grid, kThreads, smem_, st>>>(rpt, col, (const T*)val, (const T*)x, (T*)y, r0,   \
                                             r1, order, cl, rl, n_rows);                        \
     } while (0)
