@@ -37,7 +37,7 @@ EXPORTED = (
     "sellb_coo_to_crs", "sellb_mm_parse_body", "sellb_mm_format_body",
     "sellb_launch_count", "sellb_long_info", "sellb_streamed_bytes",
     "sellb_lru_stream_misses", "sellb_sell_x_lines", "sellb_host_register",
-    "sellb_host_unregister", "sellb_set_packed", "sellb_crs_import", "sellb_crs_spmv_host",
+    "sellb_host_unregister", "sellb_set_packed", "sellb_set_shadow", "sellb_crs_import", "sellb_crs_spmv_host",
     "sellb_crs_free", "sellb_gen_powerlaw_rpt", "sellb_gen_powerlaw_fill",
 )
 
@@ -52,6 +52,7 @@ class Info(ctypes.Structure):
         ("device", ctypes.c_int32), ("col_permuted", ctypes.c_int32),
         ("variant", ctypes.c_int32), ("has_row_lengths", ctypes.c_int32),
         ("max_cl", ctypes.c_int32), ("packed", ctypes.c_int32),
+        ("shadow", ctypes.c_int32),
     ]
 
 
@@ -78,6 +79,7 @@ _PROTOS = {
     "sellb_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32]),
     "sellb_set_variant": (ctypes.c_int, [_vp, _i32]),
     "sellb_set_packed": (ctypes.c_int, [_vp, _i32]),
+    "sellb_set_shadow": (ctypes.c_int, [_vp, _i32]),
     "sellb_crs_import": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _i32,
                                         ctypes.POINTER(_vp)]),
     "sellb_crs_spmv_host": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _i32]),

@@ -284,6 +284,7 @@ void free_mat_arrays(sellb_mat* m) {
     cudaFree(m->prpt);
     cudaFree(m->pcol);
     cudaFree(m->pval);
+    free_shadow(m);
     if (m->pipe_ready) {
         cudaStreamDestroy(m->s_h2d);
         cudaStreamDestroy(m->s_comp);
@@ -702,6 +703,141 @@ int build_packed(sellb_mat* m, cudaStream_t st, int force) {
 
 }  // namespace sellb
 
+namespace {
+
+// ---------------------------------------------------------------------------
+// Shadow execution layout.  Per-row sums do not depend on where a row is
+// stored: SELL-32-N (every row sorted by length, chunks of near-equal rows)
+// streams an irregular matrix with almost no padding, its longest rows
+// together in the first chunks.  The shadow holds the caller's stored rows
+// re-laid that way; a full-range SpMV runs on it and scatters each sum to the
+// caller's stored (or original) row through sh_ord_*, adding the reference's
+// 0 * x[0] term where the CALLER's chunk padded the row (bit 31).  The
+// caller's arrays stay the exported layout.
+// ---------------------------------------------------------------------------
+__global__ void k_shadow_maps(const int32_t* __restrict__ sh_order, int64_t sh_rows,
+                              int64_t sh_pad, const int32_t* __restrict__ rl,
+                              const int32_t* __restrict__ cl, int64_t C,
+                              const int32_t* __restrict__ order, int64_t n_rows, int64_t n_pad,
+                              int32_t* __restrict__ ord_st, int32_t* __restrict__ ord_or) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= sh_pad) return;
+    const int64_t p = q < sh_rows ? sh_order[q] : n_pad;
+    if (p >= n_pad) {
+        ord_st[q] = 0x7fffffff;
+        ord_or[q] = 0x7fffffff;
+        return;
+    }
+    const uint32_t flag = rl[p] < cl[p / C] ? 0x80000000u : 0u;
+    int64_t t = order ? (int64_t)order[p] : p;
+    if (t >= n_rows) t = 0x7fffffff;
+    ord_st[q] = (int32_t)((uint32_t)p | flag);
+    ord_or[q] = (int32_t)((uint32_t)t | flag);
+}
+
+}  // namespace
+
+namespace sellb {
+
+void free_shadow(sellb_mat* m) {
+    if (m->shadow) {
+        free_mat_arrays(m->shadow);
+        delete m->shadow;
+    }
+    cudaFree(m->sh_ord_st);
+    cudaFree(m->sh_ord_or);
+    m->shadow = nullptr;
+    m->sh_ord_st = nullptr;
+    m->sh_ord_or = nullptr;
+}
+
+// force: 1 build, 0 drop, -1 cost model, -2 the build's default (the cost
+// model unless SELLB_SHADOW says 0 / 1).  Cost model: build when the layout is
+// irregular (chunk occupancy beta < 0.9), not already SELL-32-N, and x fits
+// the L2 comfortably (the global sort scatters rows; with x in L2 the gathers
+// do not care where a row sits)
+int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
+    static thread_local bool building = false;
+    if (building) return 0;                       // the shadow's own build
+    free_shadow(m);
+    bool from_env = false;
+    if (force == -2) {
+        const char* e = getenv("SELLB_SHADOW");
+        force = (!e || strcmp(e, "auto") == 0) ? -1 : (atoi(e) ? 1 : 0);
+        from_env = true;
+    }
+    if (force == 0) return 0;
+    const bool possible = m->rl && m->n_rows > 0 && m->nnz > 0 && m->n_chunks > 0 &&
+                          m->n_pad < (1LL << 31) - 64;
+    if (!possible) {
+        if (force == 1 && !from_env)
+            return set_error(SELLB_EPARAM, "the shadow layout needs row_lengths and entries");
+        return 0;
+    }
+    const int64_t vs = (int64_t)vsize(m->dtype);
+    if (force < 0) {
+        const double beta = m->slots ? (double)m->nnz / (double)m->slots : 1.0;
+        const bool sorted = m->C == 32 && m->sigma_eff >= m->n_pad;
+        double x_max = 48.0 * (1 << 20);
+        if (const char* e = getenv("SELLB_SHADOW_X_MAX")) x_max = atof(e);
+        if (sorted || beta >= 0.9 || (double)m->n_cols * (double)vs > x_max) return 0;
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+        if (2.0 * (double)m->nnz * (double)(vs + 4) > 0.5 * (double)free_b) return 0;
+    }
+    // 1. the caller's stored rows as a CRS (every row, slot order)
+    const int64_t n = m->n_pad;
+    DBuf d_len, d_rpt, d_col, d_val, d_tmp;
+    SELLB_CU(d_len.alloc((n + 1) * 8, st));
+    SELLB_CU(d_rpt.alloc((n + 1) * 8, st));
+    SELLB_CU(cudaMemsetAsync(d_len.p, 0, 8, st));
+    k_packed_len<<<(unsigned)grid_for(n, 256), 256, 0, st>>>(m->rl, m->cl, nullptr, 0x7fffffff, n,
+                                                             m->C, d_len.as<int64_t>() + 1);
+    size_t tmp_bytes = 0;
+    SELLB_CU(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_len.as<int64_t>(),
+                                           d_rpt.as<int64_t>(), n + 1, st));
+    SELLB_CU(d_tmp.alloc(tmp_bytes, st));
+    SELLB_CU(cub::DeviceScan::InclusiveSum(d_tmp.p, tmp_bytes, d_len.as<int64_t>(),
+                                           d_rpt.as<int64_t>(), n + 1, st));
+    SELLB_CU(d_col.alloc(m->nnz * 4, st));
+    SELLB_CU(d_val.alloc(m->nnz * vs, st));
+    const unsigned grid = (unsigned)grid_for(n * 32, 256);
+    if (m->dtype == SELLB_F32)
+        k_packed_fill<float><<<grid, 256, 0, st>>>(m->cs, m->rl, m->col, (const float*)m->val, n,
+                                                  m->C, d_rpt.as<int64_t>(), d_col.as<int32_t>(),
+                                                  d_val.as<float>());
+    else
+        k_packed_fill<double><<<grid, 256, 0, st>>>(m->cs, m->rl, m->col, (const double*)m->val,
+                                                   n, m->C, d_rpt.as<int64_t>(),
+                                                   d_col.as<int32_t>(), d_val.as<double>());
+    if (int rc = check_stream_error()) return rc;
+    // 2. SELL-32-N of those rows (the device builder: stable sort by length)
+    sellb_mat* sh = nullptr;
+    building = true;
+    const int rc_b = sellb_build_from_crs(d_rpt.as<int64_t>(), d_col.as<int32_t>(), d_val.p,
+                                          m->dtype, n, m->n_cols, 32, n, 1, 0, m->device, st, 1,
+                                          &sh);
+    building = false;
+    if (rc_b) return rc_b;
+    m->shadow = sh;
+    // the shadow keeps the variant its cost model chose (the pad-inclusive
+    // kernels skip its padding when x[0] is not finite) and never a packed
+    // copy of its own
+    if (sh->pcol)
+        if (int rc = build_packed(sh, st, 0)) { free_shadow(m); return rc; }
+    // 3. output maps
+    if (int rc = alloc_dev((void**)&m->sh_ord_st, sh->n_pad * 4)) { free_shadow(m); return rc; }
+    if (int rc = alloc_dev((void**)&m->sh_ord_or, sh->n_pad * 4)) { free_shadow(m); return rc; }
+    k_shadow_maps<<<(unsigned)grid_for(sh->n_pad, 256), 256, 0, st>>>(
+        sh->order, sh->n_rows, sh->n_pad, m->rl, m->cl, m->C, m->order, m->n_rows, m->n_pad,
+        m->sh_ord_st, m->sh_ord_or);
+    if (int rc = check_stream_error()) { free_shadow(m); return rc; }
+    SELLB_CU(cudaStreamSynchronize(st));
+    return 0;
+}
+
+}  // namespace sellb
+
 // ===========================================================================
 // ABI
 // ===========================================================================
@@ -922,6 +1058,7 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
     if (int rc = build_long_rows(m, st)) return rc;
     if (int rc = build_packed(m, st, -2)) return rc;
+    if (int rc = build_shadow(m, st, -2)) return rc;
     SELLB_CU(cudaStreamSynchronize(st));
     holder.m = nullptr;
     *out = m;
@@ -1054,6 +1191,7 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
         if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
         if (int rc = build_long_rows(m, st)) return rc;
     if (int rc = build_packed(m, st, -2)) return rc;
+    if (int rc = build_shadow(m, st, -2)) return rc;
     } else {
         m->nnz = -1;   // unknown without row_lengths
         m->variant = SELLB_VARIANT_PAD_INCL;
@@ -1073,6 +1211,7 @@ int sellb_info(const sellb_mat* m, sellb_info_t* info) {
     info->col_permuted = m->col_permuted; info->variant = m->variant;
     info->has_row_lengths = m->rl != nullptr; info->max_cl = m->max_cl;
     info->packed = m->pcol != nullptr;
+    info->shadow = m->shadow != nullptr;
     return 0;
 }
 
@@ -1179,6 +1318,7 @@ int sellb_infer_row_lengths(sellb_mat* m, void* stream) {
     if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
     if (int rc = build_long_rows(m, st)) return rc;
     if (int rc = build_packed(m, st, -2)) return rc;
+    if (int rc = build_shadow(m, st, -2)) return rc;
     return 0;
 }
 
@@ -1203,6 +1343,14 @@ int sellb_set_packed(sellb_mat* m, int32_t mode) {
     return build_packed(m, 0, mode);
 }
 
+int sellb_set_shadow(sellb_mat* m, int32_t mode) {
+    clear_error();
+    if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
+    if (mode < -1 || mode > 1) return set_error(SELLB_EPARAM, "shadow mode must be -1, 0 or 1");
+    DeviceGuard guard(m->device);
+    return build_shadow(m, 0, mode);
+}
+
 void sellb_free(sellb_mat* m) {
     if (!m) return;
     free_mat_arrays(m);
@@ -1222,6 +1370,14 @@ int sellb_streamed_bytes(const sellb_mat* m, int64_t* matrix_bytes, int64_t* mat
     DeviceGuard guard(m->device);
     cudaStream_t st = (cudaStream_t)stream;
     const int vs = (int)vsize(m->dtype);
+    if (m->shadow) {
+        // whole-matrix SpMVs read the shadow layout plus one map entry per row
+        if (int rc = sellb_streamed_bytes(m->shadow, matrix_bytes, matrix_bytes_64, extra_bytes,
+                                          stream))
+            return rc;
+        if (extra_bytes) *extra_bytes += 4 * m->shadow->n_pad;
+        return 0;
+    }
     if (m->pcol && m->variant == SELLB_VARIANT_PAD_SKIP) {
         // the packed stored-order copy: every entry once, contiguous; plus
         // the row offsets and the chunk widths (pad fix-up)

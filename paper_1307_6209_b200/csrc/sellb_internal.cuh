@@ -80,6 +80,15 @@ struct sellb_mat {
     int32_t* pcol = nullptr;
     void* pval = nullptr;
     int64_t n_packed = 0;
+    // shadow execution layout (sellb_build.cu build_shadow): the same rows
+    // re-laid as SELL-32-N (globally sorted by length), used for full-range
+    // SpMVs of irregular layouts.  sh_ord_st / sh_ord_or map a shadow row to
+    // the caller's stored / original output row (0x7fffffff: none), bit 31 =
+    // the row was shorter than its chunk in the caller's layout (the
+    // reference's 0 * x[0] padding term)
+    sellb_mat* shadow = nullptr;
+    int32_t* sh_ord_st = nullptr;
+    int32_t* sh_ord_or = nullptr;
     int32_t long_th = 0x7fffffff;     // chunks wider than this may hold long rows
     int32_t* chunk_th = nullptr;      // per chunk: rows longer than this are long
     // long-row kernel on a side stream, forked from / joined into the
@@ -172,6 +181,8 @@ bool is_pinned(const void* p);
 int ensure_host_mirror(void** slot, size_t bytes);
 
 int build_packed(sellb_mat* m, cudaStream_t st, int force);
+int build_shadow(sellb_mat* m, cudaStream_t st, int force);
+void free_shadow(sellb_mat* m);
 constexpr int kPackedLong = 128;      // packed copy: longer rows -> warp-per-row role
                                       // (cfg3 sigma=1, threshold 64 / 128 / 256 / 512: 515 / 539 / 512 / 486 GF/s)
 

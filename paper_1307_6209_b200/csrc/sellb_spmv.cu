@@ -121,10 +121,25 @@ __device__ __forceinline__ void store_row(T* __restrict__ y, const int32_t* __re
     if (ORD == 0) {
         T out = ACC ? Arith<T>::add(y[p], sum) : sum;
         __stcs(y + p, out);
-    } else if (p < n_rows) {
-        const int64_t o = order[p];
-        y[o] = ACC ? Arith<T>::add(y[o], sum) : sum;
+    } else if (ORD == 1) {
+        if (p < n_rows) {
+            const int64_t o = order[p];
+            y[o] = ACC ? Arith<T>::add(y[o], sum) : sum;
+        }
+    } else if (p < n_rows) {     // ORD 2: the shadow layout's flagged map
+        const int32_t o = order[p] & 0x7fffffff;
+        if (o != 0x7fffffff) y[o] = ACC ? Arith<T>::add(y[o], sum) : sum;
     }
+}
+
+// The reference's 0 * x[0] padding term applies to row p: `own` (its chunk
+// in this layout is wider than the row) or, for the shadow layout (ORD 2),
+// bit 31 of its map entry (its chunk in the caller's layout was wider)
+template <int ORD>
+__device__ __forceinline__ bool pad_term(const int32_t* __restrict__ order, int64_t p,
+                                         int64_t n_rows, bool own) {
+    if constexpr (ORD == 2) return p < n_rows && order[p] < 0;
+    else return own;
 }
 
 #ifndef SELLB_VX256
@@ -324,7 +339,8 @@ __device__ __forceinline__ void long_row_at(const T* __restrict__ vp,
         for (int s = 0; s < kSeg; ++s)
             prod[s] = (jn + s * 32 + lane < len) ? Arith<T>::mul(vn[s], xn[s]) : T(0);
     }
-    if (len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+    if (pad_term<ORD>(order, p, n_rows, len < w))
+        sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
     if (lane == 0) store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
 }
 
@@ -523,7 +539,8 @@ k_spmv_long_grp(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     }
     if (lane < 8 && s_len[r] > 0) {
         const int64_t row = g0 + r;
-        if (s_len[r] < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+        if (pad_term<ORD>(order, row, n_rows, s_len[r] < w))
+            sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
         store_row<T, ACC, ORD>(y, order, row, n_rows, sum);
     }
 }
@@ -600,6 +617,16 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     const int w = cl[chunk];
     int len = SKIP ? rl[p] : w;
     bool skip_pad = SKIP;
+    if constexpr (ORD == 2 && !SKIP) {
+        // the shadow layout, pad-inclusive: its own padding slots add
+        // 0 * x[0], an exact no-op while x[0] is finite (the sum starts at
+        // +0.0 and is never -0.0); otherwise they are skipped and only the
+        // caller's padding term (the map's bit 31) applies
+        if (!isfinite(__ldg(x))) {
+            len = rl[p];
+            skip_pad = true;
+        }
+    }
     if (LONG && w > long_th) {           // a chunk that may hold long rows
         if (!SKIP) len = rl[p];
         if (len > chunk_th[chunk]) return;   // owned by the long-row role
@@ -610,7 +637,8 @@ k_spmv_sell(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
     // vector x loads only in the C = 32 instances (the generic-C ones have
     // no registers to spare for them)
     T sum = row_sum<T, U>(vp, cp, C, len, x, pol_s, pol_x, CC == 32 && ((l2pol >> 8) & 1));
-    if (skip_pad && len < w) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+    if (pad_term<ORD>(order, p, n_rows, skip_pad && len < w))
+        sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
     store_row<T, ACC, ORD>(y, order, p, n_rows, sum);
 }
 
@@ -635,6 +663,9 @@ k_spmv_sell_short(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl
     if (cb >= c1) return;
     int64_t base[K];
     int w[K], len[K];
+    // shadow layout (ORD 2), pad-inclusive: its own padding is skipped when
+    // x[0] is not finite (see k_spmv_sell)
+    const bool own_skip = SKIP || (ORD == 2 && !isfinite(__ldg(x)));
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int64_t c = cb + k;
@@ -644,7 +675,7 @@ k_spmv_sell_short(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl
         if (c < c1) {
             base[k] = cs[c];
             w[k] = cl[c];
-            len[k] = SKIP ? rl[c * 32 + lane] : w[k];
+            len[k] = own_skip ? rl[c * 32 + lane] : w[k];
         }
     }
     T v[K][W];
@@ -672,7 +703,8 @@ k_spmv_sell_short(const int64_t* __restrict__ cs, const int32_t* __restrict__ cl
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (j < len[k]) sum = Arith<T>::add(sum, Arith<T>::mul(v[k][j], xv[k][j]));
-        if (SKIP && len[k] < w[k]) sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
+        if (pad_term<ORD>(order, (cb + k) * 32 + lane, n_rows, SKIP && len[k] < w[k]))
+            sum = Arith<T>::add(sum, Arith<T>::mul(T(0), __ldg(x)));
         store_row<T, ACC, ORD>(y, order, (cb + k) * 32 + lane, n_rows, sum);
     }
 }
@@ -1077,7 +1109,7 @@ int launch_packed(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_
 
 template <typename T, int CC, bool SKIP, bool ACC, int ORD>
 int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1,
-               cudaStream_t st) {
+               cudaStream_t st, const int32_t* ordp) {
     const int64_t rows = p1 - p0;
     if (rows <= 0) return 0;
     const int64_t n_long = m->long_rows ? m->n_long : 0;
@@ -1138,7 +1170,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
             }                                                                                   \
         }                                                                                       \
         k_spmv_sell<T, CC, SKIP, ACC, ORD, UU, LL><<<grid, bt, 0, st>>>(                        \
-            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,        \
+            m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, ordp,        \
             m->C, p0, p1, m->n_rows, LR, NL, TH, m->chunk_th, l2pol,                            \
             (SD) ? m->side_off : nullptr, (SD) ? m->side_col : nullptr,                         \
             (const T*)((SD) ? m->side_val : nullptr));                                          \
@@ -1158,7 +1190,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
 #define SELLB_SHORT_LAUNCH(KK, WW)                                                              \
     k_spmv_sell_short<T, SKIP, ACC, ORD, KK, WW>                                                \
         <<<(unsigned)((chunks + (kThreads / 32) * KK - 1) / ((kThreads / 32) * KK)), kThreads, 0, \
-           st>>>(m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,   \
+           st>>>(m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, ordp,   \
                  p0 / 32, p1 / 32, m->n_rows, l2pol)
         if (m->max_cl <= 1) SELLB_SHORT_LAUNCH(4, 1);
         else SELLB_SHORT_LAUNCH(2, 2);
@@ -1217,7 +1249,7 @@ int dispatch_u(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p
             for (int64_t g_ = 0; g_ < m->n_groups; g_ += grp_ctas) {
                 const int64_t ng_ = std::min<int64_t>(m->n_groups - g_, grp_ctas);
                 k_spmv_long_grp<T, ACC, ORD, 4, 2, 64><<<(unsigned)ng_, kGT, smem_, ls>>>(
-                    m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, m->order,
+                    m->cs, m->cl, m->rl, m->col, (const T*)m->val, (const T*)x, (T*)y, ordp,
                     m->C, p0, p1, m->n_rows, m->long_groups + g_, ng_, m->chunk_th, l2pol);
                 count_launches();
             }
@@ -1260,11 +1292,25 @@ template <typename T, int CC, bool SKIP>
 int dispatch_acc(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t p1, int acc,
                  int ord, cudaStream_t st) {
     if (acc) {
-        return ord ? dispatch_u<T, CC, SKIP, true, 1>(m, x, y, p0, p1, st)
-                   : dispatch_u<T, CC, SKIP, true, 0>(m, x, y, p0, p1, st);
+        return ord ? dispatch_u<T, CC, SKIP, true, 1>(m, x, y, p0, p1, st, m->order)
+                   : dispatch_u<T, CC, SKIP, true, 0>(m, x, y, p0, p1, st, m->order);
     }
-    return ord ? dispatch_u<T, CC, SKIP, false, 1>(m, x, y, p0, p1, st)
-               : dispatch_u<T, CC, SKIP, false, 0>(m, x, y, p0, p1, st);
+    return ord ? dispatch_u<T, CC, SKIP, false, 1>(m, x, y, p0, p1, st, m->order)
+               : dispatch_u<T, CC, SKIP, false, 0>(m, x, y, p0, p1, st, m->order);
+}
+
+// the whole matrix through its SELL-32-N shadow (build_shadow), sums
+// scattered through the flagged maps (ORD 2)
+template <typename T>
+int dispatch_shadow(const sellb_mat* m, const void* x, void* y, int acc, int ord,
+                    cudaStream_t st) {
+    const sellb_mat* sh = m->shadow;
+    const int32_t* o = ord ? m->sh_ord_or : m->sh_ord_st;
+    if (sh->variant == SELLB_VARIANT_PAD_SKIP)
+        return acc ? dispatch_u<T, 32, true, true, 2>(sh, x, y, 0, sh->n_pad, st, o)
+                   : dispatch_u<T, 32, true, false, 2>(sh, x, y, 0, sh->n_pad, st, o);
+    return acc ? dispatch_u<T, 32, false, true, 2>(sh, x, y, 0, sh->n_pad, st, o)
+               : dispatch_u<T, 32, false, false, 2>(sh, x, y, 0, sh->n_pad, st, o);
 }
 
 template <typename T>
@@ -1298,6 +1344,16 @@ int launch_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t 
     if (out_order == SELLB_ORDER_ORIGINAL && !m->order)
         return set_error(SELLB_EPARAM, "original-order output needs the row permutation");
     if (c0 == c1) return 0;
+    if (m->shadow && c0 == 0 && c1 == m->n_chunks) {
+        const int ord = out_order == SELLB_ORDER_ORIGINAL;
+        int rc = m->dtype == SELLB_F32 ? dispatch_shadow<float>(m, x, y, accumulate, ord, st)
+                                       : dispatch_shadow<double>(m, x, y, accumulate, ord, st);
+        if (rc) return rc;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess)
+            return set_error(SELLB_ERESOURCE, "spmv launch failed: %s", cudaGetErrorString(e));
+        return 0;
+    }
     // TMA bulk-copy path (sellb_tma.cu) for C = 32 pad-inclusive layouts:
     // default for fp32 (cfg2: 1503 vs 1472 GF/s), slower for fp64 (914 vs
     // ~1030: too few consumer warps hide the gather latency).  SELLB_TMA=0/1

@@ -466,6 +466,18 @@ class SellMatrix:
         code = -1 if mode is None else (1 if mode else 0)
         _lib.check(_lib.load().sellb_set_packed(self.handle, code))
 
+    @property
+    def shadow(self):
+        """Whether whole-matrix SpMVs run on the SELL-32-N shadow layout
+        (irregular layouts with x in L2; the exported arrays are unchanged)."""
+        return bool(self.info().shadow)
+
+    def set_shadow(self, mode):
+        """True builds the shadow layout, False drops it, None lets the
+        build's cost model decide (sellb_set_shadow)."""
+        code = -1 if mode is None else (1 if mode else 0)
+        _lib.check(_lib.load().sellb_set_shadow(self.handle, code))
+
     def set_variant(self, name):
         code = {"auto": _lib.VARIANT_AUTO, "pad_skip": _lib.VARIANT_PAD_SKIP,
                 "pad_incl": _lib.VARIANT_PAD_INCL}.get(name)

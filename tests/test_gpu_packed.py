@@ -21,6 +21,13 @@ pytestmark = pytest.mark.gpu
 ARRAYS = ("cs", "cl", "col", "val", "perm", "row_lengths")
 
 
+@pytest.fixture(autouse=True)
+def _caller_layout(monkeypatch):
+    """These tests target the kernels on the caller's own layout: no shadow
+    layout (test_gpu_shadow.py covers that one)."""
+    monkeypatch.setenv("SELLB_SHADOW", "0")
+
+
 @pytest.fixture(scope="module", autouse=True)
 def _need_gpu():
     if not sb.HAS_CUDA:

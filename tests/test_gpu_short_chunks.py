@@ -16,6 +16,13 @@ pytestmark = pytest.mark.gpu
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.fixture(autouse=True)
+def _caller_layout(monkeypatch):
+    """These tests target the kernels on the caller's own layout: no shadow
+    layout (test_gpu_shadow.py covers that one)."""
+    monkeypatch.setenv("SELLB_SHADOW", "0")
+
+
 @pytest.fixture(scope="module", autouse=True)
 def _need_gpu():
     if not sb.HAS_CUDA:
