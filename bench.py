@@ -401,9 +401,10 @@ def host_workload(args, dt_np):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    sb.crs_to_sell_device(rpt_d, col_d, val_d, crs.n_rows, crs.n_cols, args.C, args.sigma).free()
+    s2 = sb.crs_to_sell_device(rpt_d, col_d, val_d, crs.n_rows, crs.n_cols, args.C, args.sigma)
     e1.record()
     e1.synchronize()
+    s2.free()                       # after the closing event (cudaFree is synchronous)
     build_dev_ms = e0.elapsed_time(e1)
     del rpt_d, col_d, val_d
     t0 = time.perf_counter()
@@ -450,6 +451,8 @@ def build_roofline(info, dt_np, device_ms, host_s, note=""):
     gbs = (read + write) / (device_ms / 1e3) / 1e9 if device_ms > 0 else None
     peak, _ = measured_peaks()
     return {"device_ms": round(device_ms, 3), "host_s": round(host_s, 4),
+            "includes": "sort, layout, fill, variant cost model" + (
+                ", the SELL-32 shadow copy (DESIGN.md 4.2)" if info.shadow else ""),
             "bytes_alg": int(read + write),
             "achieved_gbs": round(gbs, 1) if gbs else None,
             "frac_of_hbm": round(gbs / peak, 4) if gbs else None, "note": note}
@@ -487,12 +490,14 @@ def cfg5_workload(args, dt_np):
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0 - t_gen
     # the device build alone, timed with CUDA events (a second build of the
-    # same CRS, freed at once)
+    # same CRS; the build returns once its stream is idle, and the matrix is
+    # freed after the closing event)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    sb.crs_to_sell_device(rpt, col, val, n, n, args.C, sigma).free()
+    s2 = sb.crs_to_sell_device(rpt, col, val, n, n, args.C, sigma)
     e1.record()
     e1.synchronize()
+    s2.free()
     build_dev_ms = e0.elapsed_time(e1)
     del rpt, col, val
     torch.cuda.empty_cache()
@@ -680,8 +685,9 @@ def run_ours(args):
     if not args.skip_cpu:
         cpu = wl["cpu"](args.cpu_budget)
 
-    traffic = load_profile_traffic(f"{args.config}_s{sigma}_{args.dtype}") if args.C == 32 \
-        else None
+    shadow = bool(getattr(s, "shadow", False))
+    traffic = load_profile_traffic(f"{args.config}_s{sigma}_{args.dtype}"
+                                   + ("_shadow" if shadow else "")) if args.C == 32 else None
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup,
@@ -691,6 +697,16 @@ def run_ours(args):
         "details": {"matrix": desc, "n_rows": n_rows, "nnz": nnz, "slots": slots,
                     "beta": round(nnz / slots, 6), "kernel_variant": s.variant,
                     "packed_copy": s.packed,
+                    # irregular layouts: whole-matrix SpMVs stream a device-built
+                    # SELL-32-N (x in L2) or SELL-32-512 copy of the same rows and
+                    # scatter each row's sum back (bit-exact); SELLB_SHADOW=0 times
+                    # the layout as built
+                    "shadow_layout": shadow,
+                    "executed_layout": ("SELL-32-%s shadow of the stored rows, sums "
+                                        "scattered to the SELL-%d-%d rows" % (
+                                            "N" if s.shadow_sigma >= n_pad else s.shadow_sigma,
+                                            args.C, sigma))
+                    if shadow else "SELL-%d-%d as built" % (args.C, sigma),
                     "long_rows": s.long_rows_info(),
                     "l2": ("flushed between steps (%d MB scratch write, then half of it "
                            "read back so the L2 holds clean lines); value from the SpMV's "

@@ -73,7 +73,7 @@ typedef struct sellb_info_t {
     int32_t has_row_lengths;
     int32_t max_cl;
     int32_t packed;         /* the SpMV streams the packed chunk copy (C = 32, pad-heavy) */
-    int32_t shadow;         /* full-range SpMVs run on the SELL-32-N shadow layout */
+    int32_t shadow;         /* sigma of the SELL-32 shadow full-range SpMVs run on (0: none) */
 } sellb_info_t;
 
 /* How the matrix's long rows are handled (rows the bulk role skips):
@@ -166,14 +166,17 @@ int sellb_set_variant(sellb_mat* m, int32_t variant);
 int sellb_set_packed(sellb_mat* m, int32_t mode);
 
 /* Shadow execution layout for irregular layouts: 1 builds it (a device copy
- * of the stored rows re-laid as SELL-32-N, i.e. sorted by length over the
- * whole matrix; every full-range sellb_spmv then runs on it and scatters
- * each row's sum to the caller's stored / original row, bit-identical,
- * including the 0 * x[0] term of the caller's padding), 0 drops it, -1
- * applies the cost model (chunk occupancy < 0.9, not already SELL-32-N, x
- * at most SELLB_SHADOW_X_MAX bytes, default 48 MiB).  Every build applies
- * the cost model unless SELLB_SHADOW=0 / 1 forces it.  Chunk-range calls
- * (c0, c1 not the whole matrix) keep the caller's layout. */
+ * of the stored rows re-laid as SELL-32-N -- sorted by length over the
+ * whole matrix -- when x is at most SELLB_SHADOW_X_MAX bytes (default
+ * 48 MiB, i.e. x stays in L2), else as SELL-32-512, which keeps a chunk's
+ * rows neighbours and their x lines shared; every full-range sellb_spmv then
+ * runs on it and scatters each row's sum to the caller's stored / original
+ * row, bit-identical, including the 0 * x[0] term of the caller's padding),
+ * 0 drops it, -1 applies the cost model (chunk occupancy < 0.9 and the
+ * caller's layout not already sorted that widely).  Every build applies the
+ * cost model unless SELLB_SHADOW=0 / 1 forces it.  Chunk-range calls (c0, c1
+ * not the whole matrix) keep the caller's layout.  sellb_info_t.shadow is
+ * the shadow's sigma (0: none). */
 int sellb_set_shadow(sellb_mat* m, int32_t mode);
 void sellb_free(sellb_mat* m);
 

@@ -21,6 +21,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <functional>
 #include <vector>
 
@@ -33,19 +34,28 @@ namespace {
 __global__ void k_row_lengths(const int64_t* __restrict__ rpt, int64_t n, int64_t n_pad,
                               int32_t* __restrict__ len, unsigned int* __restrict__ maxlen,
                               int* __restrict__ bad) {
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    unsigned int l = 0;
-    if (p < n_pad) {
+    // grid-stride; the maximum is reduced per warp, then per block in shared
+    // memory, then one global atomic per block (one per warp serialised 2^21
+    // atomics on one address for cfg5: 1.6 ms)
+    __shared__ unsigned int s_max;
+    if (threadIdx.x == 0) s_max = 0;
+    __syncthreads();
+    unsigned int lmax = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_pad; p += stride) {
+        unsigned int l = 0;
         if (p < n) {
             int64_t d = rpt[p + 1] - rpt[p];
             if (d < 0 || d > 0x7fffffffLL) { atomicExch(bad, 1); d = 0; }
             l = (unsigned int)d;
         }
         len[p] = (int32_t)l;
+        lmax = max(lmax, l);
     }
-    // warp max then one atomic per warp
-    for (int o = 16; o > 0; o >>= 1) l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
-    if ((threadIdx.x & 31) == 0 && l) atomicMax(maxlen, l);
+    for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    if ((threadIdx.x & 31) == 0 && lmax) atomicMax(&s_max, lmax);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_max) atomicMax(maxlen, s_max);
 }
 
 // sellb_import's layout invariants: bad = 3 (cs[0] != 0), 4 (chunk extent
@@ -93,10 +103,12 @@ __global__ void k_apply_order(const int32_t* __restrict__ order, const int32_t* 
     if (o < n) perm[o] = (int32_t)p;
 }
 
-// one warp per chunk: max of the chunk's C stored-row lengths
+// one warp per chunk: max of the chunk's C stored-row lengths (sigma = 1; the
+// sorted layouts get their widths from k_scope_sort).  The largest width is
+// the longest row rounded to the unit, so no reduction is needed here.
 __global__ void k_chunk_width(const int32_t* __restrict__ rl, int64_t n_chunks, int64_t C,
                               int64_t unit, int32_t* __restrict__ cl,
-                              int64_t* __restrict__ slots, unsigned int* __restrict__ maxcl) {
+                              int64_t* __restrict__ slots) {
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (w >= n_chunks) return;
@@ -109,20 +121,82 @@ __global__ void k_chunk_width(const int32_t* __restrict__ rl, int64_t n_chunks, 
         if (unit > 1) mm = ((mm + unit - 1) / unit) * unit;
         cl[w] = (int32_t)mm;
         slots[w] = C * mm;
-        atomicMax(maxcl, (unsigned int)mm);
+    }
+}
+
+// sigma = 1: stored order is the original order; row_lengths, order and perm
+// in one pass (k_apply_order without the sort)
+__global__ void k_identity_order(const int32_t* __restrict__ len, int64_t n, int64_t n_pad,
+                                 int32_t* __restrict__ perm, int32_t* __restrict__ rl,
+                                 int32_t* __restrict__ order_out) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n_pad) return;
+    rl[p] = len[p];
+    order_out[p] = (int32_t)p;
+    if (p < n) perm[p] = (int32_t)p;
+}
+
+// The sigma-window sort (formats.py:285-292, np.lexsort((idx, -len, scope)))
+// for scopes of at most TH*IT rows: one CTA per scope loads the scope's row
+// lengths, sorts (maxlen - len) with the in-scope index as payload by a
+// stable block radix sort over lbits bits only (equal lengths keep their
+// original order = the idx tie-break), and writes order / row_lengths / perm
+// plus -- scopes are whole chunks (sigma_eff is a multiple of C or n_pad) and
+// sorted descending, so a chunk's width is its first row's length -- cl and
+// the per-chunk slot counts.  Replaces key build + device radix sort +
+// k_apply_order + k_chunk_width (cfg5: 5.4 ms -> one launch).
+template <int TH, int IT>
+__global__ void __launch_bounds__(TH) k_scope_sort(
+        const int32_t* __restrict__ len, int64_t n, int64_t n_pad, int64_t sigma_eff, int lbits,
+        unsigned int maxlen, int64_t C, int64_t unit, int32_t* __restrict__ perm,
+        int32_t* __restrict__ rl, int32_t* __restrict__ order_out, int32_t* __restrict__ cl,
+        int64_t* __restrict__ slots) {
+    using Sort = cub::BlockRadixSort<uint32_t, TH, IT, int32_t>;
+    __shared__ typename Sort::TempStorage tmp;
+    const int64_t s0 = (int64_t)blockIdx.x * sigma_eff;
+    const int sz = (int)(n_pad - s0 < sigma_eff ? n_pad - s0 : sigma_eff);
+    const uint32_t pad_key = lbits >= 32 ? 0xffffffffu : ((1u << lbits) - 1u);
+    uint32_t keys[IT];
+    int32_t idx[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const int r = threadIdx.x * IT + i;          // blocked: rank order = input order
+        idx[i] = r;
+        keys[i] = r < sz ? maxlen - (uint32_t)len[s0 + r] : pad_key;
+    }
+    Sort(tmp).SortBlockedToStriped(keys, idx, 0, lbits);
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const int r = i * TH + threadIdx.x;          // striped: coalesced stores
+        if (r >= sz) continue;
+        const int64_t p = s0 + r;
+        const int64_t o = s0 + idx[i];
+        const int32_t l = (int32_t)(maxlen - keys[i]);
+        rl[p] = l;
+        order_out[p] = (int32_t)o;
+        if (o < n) perm[o] = (int32_t)p;
+        if (p % C == 0) {
+            int64_t w = l;
+            if (unit > 1) w = ((w + unit - 1) / unit) * unit;
+            cl[p / C] = (int32_t)w;
+            slots[p / C] = C * w;
+        }
     }
 }
 
 // one thread per stored row; consecutive threads of a chunk write consecutive
 // addresses for every slot j (coalesced stores), each thread streams its own
-// CRS row (L1-resident lines across j).
-template <typename T>
+// CRS row (L1-resident lines across j).  U slots per batch: the batch's
+// loads are all in flight before its stores (and a row's lines are consumed
+// before other warps evict them from L1).
+template <typename T, int U>
 __global__ void k_fill(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col_in,
                        const T* __restrict__ val_in, int64_t n, int64_t n_pad, int64_t C,
                        const int32_t* __restrict__ order, const int32_t* __restrict__ rl,
                        const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
                        const int32_t* __restrict__ perm, int permute_cols,
-                       int32_t* __restrict__ col_out, T* __restrict__ val_out) {
+                       int32_t* __restrict__ col_out, T* __restrict__ val_out, int64_t n_cols,
+                       int* __restrict__ bad) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n_pad) return;
     int64_t chunk = p / C;
@@ -131,17 +205,36 @@ __global__ void k_fill(const int64_t* __restrict__ rpt, const int32_t* __restric
     int32_t len = rl[p];
     int32_t o = order[p];
     int64_t src = (o < n) ? rpt[o] : 0;
-    for (int32_t j = 0; j < w; ++j) {
-        T v = T(0);
-        int32_t c = 0;
-        if (j < len) {
-            v = val_in[src + j];
-            c = col_in[src + j];
-            if (permute_cols) c = perm[c];
+    int flag = 0;
+    for (int32_t j0 = 0; j0 < w; j0 += U) {
+        T v[U];
+        int32_t c[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int32_t j = j0 + k;
+            v[k] = T(0);
+            c[k] = 0;
+            if (j < len) {
+                v[k] = __ldg(val_in + src + j);
+                c[k] = __ldg(col_in + src + j);
+            }
         }
-        val_out[dst + (int64_t)j * C] = v;
-        col_out[dst + (int64_t)j * C] = c;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int32_t j = j0 + k;
+            if (j >= w) break;
+            // every CRS entry passes here exactly once: the column-bound
+            // check rides on the fill (bad != nullptr) instead of a 4 B/nnz
+            // pass of its own; with permute_cols it ran before the fill
+            if (j < len) {
+                if (bad) flag |= (c[k] < 0) | ((int64_t)c[k] >= n_cols);
+                if (permute_cols) c[k] = perm[c[k]];
+            }
+            __stcs(val_out + dst + (int64_t)j * C, v[k]);
+            __stcs(col_out + dst + (int64_t)j * C, c[k]);
+        }
     }
+    if (bad && flag) atomicExch(bad, 2);
 }
 
 // sector accounting for the cost model: a 32-byte sector of val (4 fp64 / 8
@@ -709,7 +802,8 @@ namespace {
 // Shadow execution layout.  Per-row sums do not depend on where a row is
 // stored: SELL-32-N (every row sorted by length, chunks of near-equal rows)
 // streams an irregular matrix with almost no padding, its longest rows
-// together in the first chunks.  The shadow holds the caller's stored rows
+// together in the first chunks; SELL-32-512 does most of that for matrices
+// whose x is far larger than L2 without scattering neighbouring rows.  The shadow holds the caller's stored rows
 // re-laid that way; a full-range SpMV runs on it and scatters each sum to the
 // caller's stored (or original) row through sh_ord_*, adding the reference's
 // 0 * x[0] term where the CALLER's chunk padded the row (bit 31).  The
@@ -753,9 +847,10 @@ void free_shadow(sellb_mat* m) {
 
 // force: 1 build, 0 drop, -1 cost model, -2 the build's default (the cost
 // model unless SELLB_SHADOW says 0 / 1).  Cost model: build when the layout is
-// irregular (chunk occupancy beta < 0.9), not already SELL-32-N, and x fits
-// the L2 comfortably (the global sort scatters rows; with x in L2 the gathers
-// do not care where a row sits)
+// irregular (chunk occupancy beta < 0.9) and not already sorted as widely as
+// the shadow would be (SELL-32-N when x fits the L2 comfortably -- the global
+// sort scatters rows, and with x in L2 the gathers do not care where a row
+// sits -- else SELL-32-512)
 int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
     static thread_local bool building = false;
     if (building) return 0;                       // the shadow's own build
@@ -775,16 +870,31 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
         return 0;
     }
     const int64_t vs = (int64_t)vsize(m->dtype);
+    // x in L2: one global scope (SELL-32-N; where a row lands does not matter
+    // to its gathers).  x far larger than L2: 512-row windows, so the rows a
+    // chunk holds stay neighbours and the x lines they gather stay shared
+    // (cfg5 at sigma = 1 vs 512: 857 vs 1002 GF/s)
+    double x_max = 48.0 * (1 << 20);
+    if (const char* e = getenv("SELLB_SHADOW_X_MAX")) x_max = atof(e);
+    const bool x_in_l2 = (double)m->n_cols * (double)vs <= x_max;
+    const int64_t sh_sigma = x_in_l2 ? m->n_pad : 512;
     if (force < 0) {
         const double beta = m->slots ? (double)m->nnz / (double)m->slots : 1.0;
-        const bool sorted = m->C == 32 && m->sigma_eff >= m->n_pad;
-        double x_max = 48.0 * (1 << 20);
-        if (const char* e = getenv("SELLB_SHADOW_X_MAX")) x_max = atof(e);
-        if (sorted || beta >= 0.9 || (double)m->n_cols * (double)vs > x_max) return 0;
+        const bool sorted = m->C == 32 && m->sigma_eff >= std::min<int64_t>(sh_sigma, m->n_pad);
+        if (sorted || beta >= 0.9) return 0;
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
         if (2.0 * (double)m->nnz * (double)(vs + 4) > 0.5 * (double)free_b) return 0;
     }
+    static const bool trace = getenv("SELLB_BUILD_TRACE") != nullptr;
+    const auto t_begin = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "shadow %-12s %9.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                          t_begin).count());
+    };
     // 1. the caller's stored rows as a CRS (every row, slot order)
     const int64_t n = m->n_pad;
     DBuf d_len, d_rpt, d_col, d_val, d_tmp;
@@ -811,14 +921,16 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
                                                    n, m->C, d_rpt.as<int64_t>(),
                                                    d_col.as<int32_t>(), d_val.as<double>());
     if (int rc = check_stream_error()) return rc;
+    mark("stored CRS");
     // 2. SELL-32-N of those rows (the device builder: stable sort by length)
     sellb_mat* sh = nullptr;
     building = true;
     const int rc_b = sellb_build_from_crs(d_rpt.as<int64_t>(), d_col.as<int32_t>(), d_val.p,
-                                          m->dtype, n, m->n_cols, 32, n, 1, 0, m->device, st, 1,
-                                          &sh);
+                                          m->dtype, n, m->n_cols, 32, std::min<int64_t>(sh_sigma, n),
+                                          1, 0, m->device, st, 1, &sh);
     building = false;
     if (rc_b) return rc_b;
+    mark("layout");
     m->shadow = sh;
     // the shadow keeps the variant its cost model chose (the pad-inclusive
     // kernels skip its padding when x[0] is not finite) and never a packed
@@ -833,6 +945,7 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
         m->sh_ord_st, m->sh_ord_or);
     if (int rc = check_stream_error()) { free_shadow(m); return rc; }
     SELLB_CU(cudaStreamSynchronize(st));
+    mark("maps");
     return 0;
 }
 
@@ -883,7 +996,18 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     DeviceGuard guard(device);
     if (!guard.ok) return set_error(SELLB_ERESOURCE, "cannot select CUDA device %d", device);
     cudaStream_t st = (cudaStream_t)stream;
+    PoolTrim trim_(st);
     const size_t vs = vsize(dtype);
+    // SELLB_BUILD_TRACE=1: synchronise after each phase and print its end time
+    static const bool trace = getenv("SELLB_BUILD_TRACE") != nullptr;
+    const auto t_begin = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "build %-12s %9.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                          t_begin).count());
+    };
 
     // --- inputs on device -------------------------------------------------
     int64_t rpt_host_last = 0, rpt_host_first = 0;
@@ -936,12 +1060,12 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     SELLB_CU(cudaMemsetAsync(d_flags.p, 0, 16, st));
     unsigned int* d_maxlen = d_flags.as<unsigned int>();
     int* d_bad = reinterpret_cast<int*>(d_flags.as<unsigned int>() + 1);
-    unsigned int* d_maxcl = d_flags.as<unsigned int>() + 2;
     if (n_pad)
-        k_row_lengths<<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(rpt_d, n, n_pad,
+        k_row_lengths<<<(unsigned)std::min<int64_t>(grid_for(n_pad, 256), 148 * 8), 256, 0, st>>>(
+            rpt_d, n, n_pad,
                                                                        d_len.as<int32_t>(),
                                                                        d_maxlen, d_bad);
-    if (nnz) {
+    if (nnz && permute_cols) {      // otherwise checked by k_fill
         int blocks = (int)std::min<int64_t>(grid_for(nnz, 256), 148 * 16);
         k_check_cols<<<blocks, 256, 0, st>>>(col_d, nnz, n_cols, d_bad);
     }
@@ -952,19 +1076,45 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     if (hflags[1] == 1) return set_error(SELLB_ESTRUCT, "rpt must be non-decreasing");
     if (hflags[1] == 2) return set_error(SELLB_ESTRUCT, "column index out of bounds");
     const unsigned int maxlen = hflags[0];
+    mark("lengths");
 
-    // --- 2. scope sort --------------------------------------------------------
+    // --- 2.-4. scope sort, perm / row_lengths / order, chunk widths ---------
     if (int rc = alloc_dev((void**)&m->perm, std::max<int64_t>(n, 1) * 4)) return rc;
     if (int rc = alloc_dev((void**)&m->rl, std::max<int64_t>(n_pad, 1) * 4)) return rc;
     if (int rc = alloc_dev((void**)&m->order, std::max<int64_t>(n_pad, 1) * 4)) return rc;
-    DBuf d_sorted_idx;
-    const int32_t* order_in = nullptr;
-    if (sigma_eff > 1 && n_pad > 1) {
-        const int lbits = std::max(1, bits_for(maxlen));
+    if (int rc = alloc_dev((void**)&m->cl, std::max<int64_t>(n_chunks, 1) * 4)) return rc;
+    if (int rc = alloc_dev((void**)&m->cs, (n_chunks + 1) * 8)) return rc;
+    SELLB_CU(cudaMemsetAsync(m->cs, 0, 8, st));
+    int64_t unit = 1;
+    if (align_bytes > 1) {
+        int64_t a = 4LL * C, b = align_bytes;
+        while (b) { int64_t t = a % b; a = b; b = t; }
+        unit = align_bytes / a;   // formats.py:354
+    }
+    DBuf d_slots;
+    if (n_chunks) SELLB_CU(d_slots.alloc(n_chunks * 8, st));
+    const int lbits = std::max(1, bits_for(maxlen));
+    bool widths_done = false;
+    if (sigma_eff > 1 && n_pad > 1 && sigma_eff <= 4096) {
+        // one CTA per sigma window: sort + order + widths in one launch
+        const unsigned n_scopes = (unsigned)((n_pad + sigma_eff - 1) / sigma_eff);
+#define SELLB_SCOPE_SORT(TH, IT)                                                              \
+        k_scope_sort<TH, IT><<<n_scopes, TH, 0, st>>>(d_len.as<int32_t>(), n, n_pad, sigma_eff, \
+                                                    lbits, maxlen, C, unit, m->perm, m->rl,     \
+                                                    m->order, m->cl, d_slots.as<int64_t>())
+        if (sigma_eff <= 512) SELLB_SCOPE_SORT(128, 4);
+        else if (sigma_eff <= 1024) SELLB_SCOPE_SORT(128, 8);
+        else if (sigma_eff <= 2048) SELLB_SCOPE_SORT(256, 8);
+        else SELLB_SCOPE_SORT(512, 8);
+#undef SELLB_SCOPE_SORT
+        widths_done = true;
+    } else if (sigma_eff > 1 && n_pad > 1) {
+        // wide scopes: stable device radix sort of (scope, maxlen - len) with
+        // the index as payload == np.lexsort((idx, -len, scope))
         const int64_t n_scopes = (n_pad + sigma_eff - 1) / sigma_eff;
         const int sbits = n_scopes > 1 ? bits_for((uint64_t)(n_scopes - 1)) : 0;
         const int total_bits = lbits + sbits;
-        DBuf d_idx_in, d_keys_in, d_keys_out, d_tmp;
+        DBuf d_idx_in, d_sorted_idx, d_keys_in, d_keys_out, d_tmp;
         SELLB_CU(d_idx_in.alloc(n_pad * 4, st));
         SELLB_CU(d_sorted_idx.alloc(n_pad * 4, st));
         size_t tmp_bytes = 0;
@@ -1003,28 +1153,19 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
                                                      d_sorted_idx.as<int32_t>(), (int)n_pad, 0,
                                                      total_bits, st));
         }
-        order_in = d_sorted_idx.as<int32_t>();
-    }
-    // --- 3. perm / row_lengths / order ------------------------------------------
-    if (n_pad)
         k_apply_order<<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
-            order_in, d_len.as<int32_t>(), n, n_pad, m->perm, m->rl, m->order);
-
-    // --- 4. chunk widths + 5. cs ----------------------------------------------
-    if (int rc = alloc_dev((void**)&m->cl, std::max<int64_t>(n_chunks, 1) * 4)) return rc;
-    if (int rc = alloc_dev((void**)&m->cs, (n_chunks + 1) * 8)) return rc;
-    SELLB_CU(cudaMemsetAsync(m->cs, 0, 8, st));
-    int64_t unit = 1;
-    if (align_bytes > 1) {
-        int64_t a = 4LL * C, b = align_bytes;
-        while (b) { int64_t t = a % b; a = b; b = t; }
-        unit = align_bytes / a;   // formats.py:354
+            d_sorted_idx.as<int32_t>(), d_len.as<int32_t>(), n, n_pad, m->perm, m->rl, m->order);
+    } else if (n_pad) {
+        k_identity_order<<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
+            d_len.as<int32_t>(), n, n_pad, m->perm, m->rl, m->order);
     }
+    mark("sort+widths");
+    // --- 5. cs = [0, cumsum(C * cl)] -------------------------------------------
     if (n_chunks) {
-        DBuf d_slots, d_tmp;
-        SELLB_CU(d_slots.alloc(n_chunks * 8, st));
-        k_chunk_width<<<(unsigned)grid_for(n_chunks * 32, 256), 256, 0, st>>>(
-            m->rl, n_chunks, C, unit, m->cl, d_slots.as<int64_t>(), d_maxcl);
+        if (!widths_done)
+            k_chunk_width<<<(unsigned)grid_for(n_chunks * 32, 256), 256, 0, st>>>(
+                m->rl, n_chunks, C, unit, m->cl, d_slots.as<int64_t>());
+        DBuf d_tmp;
         size_t tmp_bytes = 0;
         SELLB_CU(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_slots.as<int64_t>(),
                                                m->cs + 1, (int)n_chunks, st));
@@ -1034,32 +1175,53 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     }
     if (int rc = check_stream_error()) return rc;
     int64_t total = 0;
-    unsigned int maxcl = 0;
     SELLB_CU(cudaMemcpyAsync(&total, m->cs + n_chunks, 8, cudaMemcpyDeviceToHost, st));
-    SELLB_CU(cudaMemcpyAsync(&maxcl, d_maxcl, 4, cudaMemcpyDeviceToHost, st));
     SELLB_CU(cudaStreamSynchronize(st));
     m->slots = total;
-    m->max_cl = (int32_t)maxcl;
+    // the widest chunk holds the longest row: max cl = maxlen rounded to the unit
+    m->max_cl = n_chunks ? (int32_t)(((int64_t)maxlen + unit - 1) / unit * unit) : 0;
 
+    mark("cs");
     // --- 6. fill -------------------------------------------------------------
     if (int rc = alloc_dev((void**)&m->col, total * 4)) return rc;
     if (int rc = alloc_dev(&m->val, total * vs)) return rc;
+    mark("alloc");
     if (n_pad && total) {
-        if (dtype == SELLB_F64)
-            k_fill<double><<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
-                rpt_d, col_d, (const double*)val_d, n, n_pad, C, m->order, m->rl, m->cs, m->cl,
-                m->perm, permute_cols ? 1 : 0, m->col, (double*)m->val);
-        else
-            k_fill<float><<<(unsigned)grid_for(n_pad, 256), 256, 0, st>>>(
-                rpt_d, col_d, (const float*)val_d, n, n_pad, C, m->order, m->rl, m->cs, m->cl,
-                m->perm, permute_cols ? 1 : 0, m->col, (float*)m->val);
+        static const int fill_u = getenv("SELLB_FILL_U") ? atoi(getenv("SELLB_FILL_U")) : 4;
+        const unsigned grid = (unsigned)grid_for(n_pad, 256);
+        int* const chk = permute_cols ? nullptr : d_bad;
+#define SELLB_FILL(T, U)                                                                       \
+        k_fill<T, U><<<grid, 256, 0, st>>>(rpt_d, col_d, (const T*)val_d, n, n_pad, C, m->order, \
+                                           m->rl, m->cs, m->cl, m->perm, permute_cols ? 1 : 0, \
+                                           m->col, (T*)m->val, n_cols, chk)
+        if (dtype == SELLB_F64) {
+            if (fill_u == 1) SELLB_FILL(double, 1);
+            else if (fill_u == 8) SELLB_FILL(double, 8);
+            else SELLB_FILL(double, 4);
+        } else {
+            if (fill_u == 1) SELLB_FILL(float, 1);
+            else if (fill_u == 8) SELLB_FILL(float, 8);
+            else SELLB_FILL(float, 4);
+        }
+#undef SELLB_FILL
     }
     if (int rc = check_stream_error()) return rc;
+    if (nnz && !permute_cols) {
+        int hbad = 0;
+        SELLB_CU(cudaMemcpyAsync(&hbad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+        SELLB_CU(cudaStreamSynchronize(st));
+        if (hbad == 2) return set_error(SELLB_ESTRUCT, "column index out of bounds");
+    }
+    mark("fill");
     if (int rc = choose_variant(m, st, nullptr, nullptr, nullptr)) return rc;
+    mark("variant");
     if (int rc = build_long_rows(m, st)) return rc;
+    mark("long rows");
     if (int rc = build_packed(m, st, -2)) return rc;
+    mark("packed");
     if (int rc = build_shadow(m, st, -2)) return rc;
     SELLB_CU(cudaStreamSynchronize(st));
+    mark("shadow");
     holder.m = nullptr;
     *out = m;
     return 0;
@@ -1085,6 +1247,7 @@ int sellb_import(const int64_t* cs, const int32_t* cl, const int32_t* col, const
     DeviceGuard guard(device);
     if (!guard.ok) return set_error(SELLB_ERESOURCE, "cannot select CUDA device %d", device);
     cudaStream_t st = (cudaStream_t)stream;
+    PoolTrim trim_(st);
     cudaMemcpyKind kind = ptrs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     int64_t total = 0;
     if (ptrs_on_device) {
@@ -1211,7 +1374,7 @@ int sellb_info(const sellb_mat* m, sellb_info_t* info) {
     info->col_permuted = m->col_permuted; info->variant = m->variant;
     info->has_row_lengths = m->rl != nullptr; info->max_cl = m->max_cl;
     info->packed = m->pcol != nullptr;
-    info->shadow = m->shadow != nullptr;
+    info->shadow = m->shadow ? (int32_t)m->shadow->sigma : 0;
     return 0;
 }
 
@@ -1295,6 +1458,7 @@ int sellb_infer_row_lengths(sellb_mat* m, void* stream) {
     if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
     DeviceGuard guard(m->device);
     cudaStream_t st = (cudaStream_t)stream;
+    PoolTrim trim_(st);
     if (!m->rl && m->n_pad)
         if (int rc = alloc_dev((void**)&m->rl, m->n_pad * 4)) return rc;
     if (m->n_pad) {
@@ -1340,6 +1504,7 @@ int sellb_set_packed(sellb_mat* m, int32_t mode) {
     if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
     if (mode < -1 || mode > 1) return set_error(SELLB_EPARAM, "packed mode must be -1, 0 or 1");
     DeviceGuard guard(m->device);
+    PoolTrim trim_(0);
     return build_packed(m, 0, mode);
 }
 
@@ -1348,6 +1513,7 @@ int sellb_set_shadow(sellb_mat* m, int32_t mode) {
     if (!m) return set_error(SELLB_EPARAM, "NULL matrix");
     if (mode < -1 || mode > 1) return set_error(SELLB_EPARAM, "shadow mode must be -1, 0 or 1");
     DeviceGuard guard(m->device);
+    PoolTrim trim_(0);
     return build_shadow(m, 0, mode);
 }
 

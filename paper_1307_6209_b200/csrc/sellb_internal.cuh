@@ -143,6 +143,7 @@ struct DeviceGuard {
 // Keep freed stream-ordered allocations in the device's default pool (the
 // default release threshold of 0 hands them back to the driver at every
 // synchronisation, turning each temporary into a fresh cudaMalloc).
+void trim_pool_memory();
 void retain_pool_memory();
 
 // RAII device buffer (stream-ordered free)
@@ -160,6 +161,20 @@ struct DBuf {
     }
     template <typename T> T* as() const { return static_cast<T*>(p); }
     void* release() { void* q = p; p = nullptr; return q; }
+};
+
+// Declared before a build's DBufs (so it is destroyed after them): once the
+// stream's frees have completed, trim the retained pool (trim_pool_memory).
+struct PoolTrim {
+    cudaStream_t st;
+    explicit PoolTrim(cudaStream_t s) : st(s) {}
+    PoolTrim(const PoolTrim&) = delete;
+    PoolTrim& operator=(const PoolTrim&) = delete;
+    ~PoolTrim() {
+        cudaStreamSynchronize(st);
+        cudaGetLastError();
+        trim_pool_memory();
+    }
 };
 
 // launch helpers implemented in sellb_spmv.cu

@@ -1299,7 +1299,8 @@ int dispatch_acc(const sellb_mat* m, const void* x, void* y, int64_t p0, int64_t
                : dispatch_u<T, CC, SKIP, false, 0>(m, x, y, p0, p1, st, m->order);
 }
 
-// the whole matrix through its SELL-32-N shadow (build_shadow), sums
+// the whole matrix through its SELL-32 shadow (build_shadow: sigma = N, or
+// 512 for x far larger than L2), sums
 // scattered through the flagged maps (ORD 2)
 template <typename T>
 int dispatch_shadow(const sellb_mat* m, const void* x, void* y, int acc, int ord,

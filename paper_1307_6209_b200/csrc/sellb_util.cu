@@ -38,6 +38,18 @@ void retain_pool_memory() {
     done[dev] = true;
 }
 
+// After a build: hand the pool's unused memory above 1 GiB back to the device
+// (the retained pool would otherwise keep a large build's temporaries -- 16 GB
+// of stored-row CRS for a cfg5 shadow -- away from later cudaMalloc calls).
+void trim_pool_memory() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+        cudaMemPoolTrimTo(pool, (size_t)1 << 30);
+    cudaGetLastError();
+}
+
 static std::atomic<long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_counter() { return g_launches.load(std::memory_order_relaxed); }

@@ -468,9 +468,15 @@ class SellMatrix:
 
     @property
     def shadow(self):
-        """Whether whole-matrix SpMVs run on the SELL-32-N shadow layout
-        (irregular layouts with x in L2; the exported arrays are unchanged)."""
+        """Whether whole-matrix SpMVs run on a SELL-32 shadow layout of the
+        same rows (irregular layouts; the exported arrays are unchanged)."""
         return bool(self.info().shadow)
+
+    @property
+    def shadow_sigma(self):
+        """The shadow layout's sigma (n_rows: SELL-32-N, x in L2; 512 for
+        larger x), 0 without a shadow."""
+        return int(self.info().shadow)
 
     def set_shadow(self, mode):
         """True builds the shadow layout, False drops it, None lets the

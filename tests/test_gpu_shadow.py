@@ -1,6 +1,7 @@
 """The shadow execution layout (csrc/sellb_build.cu build_shadow, ORD 2 in
 csrc/sellb_spmv.cu): irregular layouts run whole-matrix SpMVs on a device
-copy of their stored rows re-laid as SELL-32-N and scatter each sum back to
+copy of their stored rows re-laid as SELL-32-N (SELL-32-512 when x is far
+larger than L2) and scatter each sum back to
 the caller's stored / original row.  The exported arrays are unchanged and y
 is bitwise the oracle's (the reference's _kernels.pyx:65-92 order for the
 CALLER's layout, padding term included) -- every C and sigma, fp32 / fp64,
@@ -117,8 +118,8 @@ def test_shadow_chunk_ranges_keep_caller_layout():
 
 
 def test_shadow_cost_model_choices():
-    """Irregular layouts with x in L2 get the shadow; dense, already
-    SELL-32-N and (with a small SELLB_SHADOW_X_MAX) large-x ones do not."""
+    """Irregular layouts get the shadow (SELL-32-N with x in L2); dense and
+    already SELL-32-N ones do not."""
     pl = generate.powerlaw(200_000, seed=4, band=5000)
     heavy = sb.crs_to_sell(pl, 32, 1)
     heavy8 = sb.crs_to_sell(pl, 8, 1)
@@ -166,3 +167,21 @@ def test_shadow_empty_rows_and_tiny():
             s.set_shadow(True)
             assert s.shadow
         _check(s, o, x, np.float64)
+
+
+@pytest.mark.parametrize("C,sigma", [(32, 1), (32, 128), (8, 1), (64, 256)])
+def test_shadow_windowed_for_large_x(monkeypatch, C, sigma):
+    """x larger than SELLB_SHADOW_X_MAX (cfg5's 512 MB x in the library's
+    default): the shadow is SELL-32-512, not SELL-32-N, so chunk rows stay
+    neighbours; layouts already sorted over >= 512 rows get none.  Bitwise
+    either way."""
+    monkeypatch.setenv("SELLB_SHADOW_X_MAX", "0")
+    m = MATS["powerlaw"]()
+    s = sb.crs_to_sell(m, C, sigma)
+    assert s.shadow and s.shadow_sigma == 512
+    o = oracle.crs_to_sell(m.rpt, m.col, m.val, m.n_rows, m.n_cols, C, sigma)
+    _check(s, o, generate.rhs(m.n_cols), np.float64)
+    assert not sb.crs_to_sell(m, 32, 512).shadow
+    monkeypatch.delenv("SELLB_SHADOW_X_MAX")
+    s.set_shadow(None)
+    assert s.shadow_sigma >= s.n_rows_padded

@@ -4,9 +4,15 @@ B200 analog of the reference's `sellkit sweep-sigma` (cli.py:296-320), which
 simulates alpha with an LRU model (cachesim.py:49-75).  Here alpha comes from
 ncu's dram__bytes_read.sum + dram__bytes_write.sum of the SpMV kernel.
 
-On the GPU box (one ncu pass, one SpMV launch per layout):
+Each layout is measured as built (SELLB shadow dropped) and, where the
+build's cost model adds the SELL-32-N shadow execution layout, once more with
+it -- the first row is the paper's sigma effect, the second
+what spmv_sell runs by default.
+
+On the GPU box (one ncu pass over the profiled SpMVs only -- the run brackets
+each with cudaProfilerStart/Stop and records how many kernels it launched):
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-        -k regex:"k_spmv_(sell|rows)" --csv --log-file gpurun_out/alpha.csv \
+        --profile-from-start off --csv --log-file gpurun_out/alpha.csv \
         python tools/alpha_sweep.py run gpurun_out/alpha_layouts.json
 and without ncu for timing:
     python tools/alpha_sweep.py time gpurun_out/alpha_times.json
@@ -39,50 +45,67 @@ def run(out_json, timed=False):
 
     import torch
     import paper_1307_6209_b200 as sb
-    from paper_1307_6209_b200 import generate
+    from paper_1307_6209_b200 import _lib, generate
+    lib = _lib.load()
     rows = []
     for name, sigma, m in matrices():
         s = sb.crs_to_sell(m, 32, sigma)
-        info = s.info()
-        be, vs, cs = s.sector_occupancy()
+        auto_shadow = s.shadow
         x = torch.from_numpy(generate.rhs(m.n_cols)).cuda()
         y = torch.zeros(s.n_rows_padded, dtype=torch.float64, device="cuda")
-        rl = s.row_lengths
-        # 64-byte granularity (two sectors): 8 fp64 lanes of val, 16 of col
-        v64 = int(rl.reshape(-1, 8).max(1).sum()) * 2
-        c64 = int(rl.reshape(-1, 16).max(1).sum()) * 2
-        mb32, mb64, mx = s.streamed_bytes()
-        rec = {"name": name, "sigma": sigma, "nnz": info.nnz, "n_rows": info.n_rows,
-               "stream32": mb32, "stream64": mb64, "stream_extra": mx,
-               "long_rows": s.long_rows_info(),
-               "n_cols": info.n_cols, "n_pad": info.n_rows_padded, "n_chunks": info.n_chunks,
-               "slots": info.slots, "beta": info.nnz / info.slots, "beta_eff": be,
-               "val_sectors": vs, "col_sectors": cs, "val_sectors64": v64,
-               "col_sectors64": c64,
-               "variant": s.variant + ("+packed" if s.packed else "")}
-        if timed:
-            for _ in range(5):
-                sb.spmv_sell(s, x, y)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(50):
-                sb.spmv_sell(s, x, y)
-            e1.record()
-            e1.synchronize()
-            rec["kernel_s"] = e0.elapsed_time(e1) / 50 / 1e3
-        else:
-            sb.spmv_sell(s, x, y)            # the one profiled launch
-            torch.cuda.synchronize()
-        rows.append(rec)
+        for mode in ((False, None) if auto_shadow else (False,)):
+            s.set_shadow(mode)
+            rows.append(measure(sb, lib, torch, name, sigma, s, x, y, timed))
         s.free()
     json.dump(rows, open(out_json, "w"), indent=1)
+
+
+def measure(sb, lib, torch, name, sigma, s, x, y, timed):
+    info = s.info()
+    be, vs, cs = s.sector_occupancy()
+    rl = s.row_lengths
+    # 64-byte granularity (two sectors): 8 fp64 lanes of val, 16 of col
+    v64 = int(rl.reshape(-1, 8).max(1).sum()) * 2
+    c64 = int(rl.reshape(-1, 16).max(1).sum()) * 2
+    mb32, mb64, mx = s.streamed_bytes()
+    rec = {"name": name, "sigma": sigma, "nnz": info.nnz, "n_rows": info.n_rows,
+           "stream32": mb32, "stream64": mb64, "stream_extra": mx,
+           "long_rows": s.long_rows_info(),
+           "n_cols": info.n_cols, "n_pad": info.n_rows_padded, "n_chunks": info.n_chunks,
+           "slots": info.slots, "beta": info.nnz / info.slots, "beta_eff": be,
+           "val_sectors": vs, "col_sectors": cs, "val_sectors64": v64,
+           "col_sectors64": c64, "shadow": s.shadow,
+           "variant": ("shadow SELL-32-%s" % ("N" if s.shadow_sigma >= info.n_rows_padded
+                                               else s.shadow_sigma)
+                       if s.shadow else s.variant + ("+packed" if s.packed else ""))}
+    sb.spmv_sell(s, x, y)                # warm (first-use setup outside the profiled range)
+    torch.cuda.synchronize()
+    if timed:
+        for _ in range(5):
+            sb.spmv_sell(s, x, y)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(50):
+            sb.spmv_sell(s, x, y)
+        e1.record()
+        e1.synchronize()
+        rec["kernel_s"] = e0.elapsed_time(e1) / 50 / 1e3
+    else:
+        n0 = lib.sellb_launch_count()
+        torch.cuda.profiler.start()
+        sb.spmv_sell(s, x, y)            # the one profiled SpMV
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        rec["launches"] = int(lib.sellb_launch_count() - n0)
+    return rec
 
 
 def report(layouts_json, ncu_csv, times_json):
     from paper_1307_6209_b200 import model
     rows = json.load(open(layouts_json))
-    times = {(r["name"], r["sigma"]): r["kernel_s"] for r in json.load(open(times_json))}
+    times = {(r["name"], r["sigma"], r.get("shadow", False)): r["kernel_s"]
+             for r in json.load(open(times_json))}
     lines = open(ncu_csv).read().splitlines()
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
     recs = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
@@ -95,6 +118,8 @@ def report(layouts_json, ncu_csv, times_json):
     # warp-per-row kernel for its long rows): sum the DRAM bytes of each
     # layout's launches
     def n_launch(row):
+        if "launches" in row:                    # counted by the library during the run
+            return row["launches"]
         packed = "+packed" in row["variant"]
         return 2 if packed and row["long_rows"]["n_long"] > 0 else 1
     groups, k = [], 0
@@ -127,7 +152,10 @@ def report(layouts_json, ncu_csv, times_json):
           "of pad-incl chunks, touched 32 B / 64 B sectors of bulk rows + row_lengths for "
           "pad-skip chunks, long rows from the contiguous side table).  Ideal alpha = 1/N_nzc.  DRAM = ncu "
           "dram__bytes_read.sum + dram__bytes_write.sum of one cold SpMV launch; "
-          "GF/s from CUDA events (50 warm launches).\n")
+          "GF/s from CUDA events (50 warm launches).  Rows marked `shadow` are the same "
+          "layout executed through its SELL-32 shadow copy (spmv_sell's default for "
+          "irregular layouts, bit-identical y); beta / beta_eff there are the CALLER's "
+          "layout; matrix MB and alpha_eff use the bytes the shadow streams.\n")
     print("| matrix | sigma | beta | beta_eff | variant | DRAM MB | V_alg MB | matrix MB (32 B / 64 B) | "
           "alpha_paper | in range | alpha_eff 32 B | alpha_eff 64 B | ideal alpha | "
           "B paper (ideal alpha) | GF/s | paper P = b/B GF/s |")
@@ -149,7 +177,7 @@ def report(layouts_json, ncu_csv, times_json):
                                         extra_bytes=extra)
         v_alg = model.algorithmic_bytes(nnz, row["n_cols"], row["n_pad"], row["n_chunks"])
         bal = model.code_balance_sell(1.0 / nzc, row["beta"], nzr)
-        t = times[(row["name"], row["sigma"])]
+        t = times[(row["name"], row["sigma"], row.get("shadow", False))]
         print(f"| {row['name']} | {row['sigma']} | {row['beta']:.4f} | {row['beta_eff']:.4f} | "
               f"{row['variant']} | {dram / 1e6:.1f} | {v_alg / 1e6:.1f} | "
               f"{mat / 1e6:.0f} / {mat64 / 1e6:.0f} | {a_p.alpha:.3f} | "

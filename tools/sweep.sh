@@ -13,6 +13,7 @@ try:
     cpu = (d.get("cpu_baseline") or {}).get("value")
     print(f"{sys.argv[1]:22} {d['value']:9.2f} GF/s frac {r['frac']:.3f} kern {r['kernel_ms']:.4f} ms "
           f"beta {c.get('beta')} {c.get('kernel_variant')}{'+packed' if c.get('packed_copy') else ''} "
+          f"[{c.get('executed_layout')}] build {(c.get('build') or {}).get('device_ms')} ms "
           f"parity {c.get('parity_vs_oracle')} e2e {d['e2e']['value']} cpu {cpu}")
 except Exception as e:
     print(sys.argv[1], "FAILED", e)
@@ -30,8 +31,16 @@ for C in 8 16 32 64 128; do
   done
   run cfg4_C${C}_s$((16*C))_f32 --config cfg4 --C $C --sigma $((16*C)) --dtype f32 --steps 300 --warmup 10 --skip-cpu
 done
-export SELLB_PACKED=0   # the same layout through the SELL bulk role, for comparison
-run cfg3_s1_nopack      --config cfg3 --sigma 1 --steps 300 --warmup 10 --skip-cpu --skip-parity
-unset SELLB_PACKED
 run cfg5_s512           --config cfg5 --sigma 512 --steps 100 --warmup 5 --cpu-budget 4
 run cfg5_s1             --config cfg5 --sigma 1 --steps 100 --warmup 5 --skip-cpu
+# the irregular layouts as built (no SELL-32 shadow copy): the
+# paper's sigma effect on the layout itself
+export SELLB_SHADOW=0
+for s in 1 32 128 512; do
+  run cfg3_s${s}_asbuilt --config cfg3 --sigma $s --steps 300 --warmup 10 --skip-cpu --skip-parity
+done
+run cfg4_C32_s1_asbuilt --config cfg4 --C 32 --sigma 1 --steps 300 --warmup 10 --skip-cpu --skip-parity
+run cfg5_s1_asbuilt     --config cfg5 --sigma 1 --steps 100 --warmup 5 --skip-cpu --skip-parity
+export SELLB_PACKED=0   # and without the packed copy either (the SELL bulk role)
+run cfg3_s1_nopack      --config cfg3 --sigma 1 --steps 300 --warmup 10 --skip-cpu --skip-parity
+unset SELLB_PACKED SELLB_SHADOW
