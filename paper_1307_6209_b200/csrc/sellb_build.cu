@@ -704,7 +704,12 @@ namespace sellb {
 // model unless SELLB_PACKED says 0 / 1 (measured, tools/packed_ab.sh: cfg3
 // sigma=1 324 -> 450 GF/s; sigma=128 / 512 and cfg4 are faster in the SELL
 // bulk role, and the model leaves them there)
+// set while build_shadow builds the shadow's own layout: that build adds
+// neither a packed copy nor a shadow of its own
+thread_local bool t_shadow_build = false;
+
 int build_packed(sellb_mat* m, cudaStream_t st, int force) {
+    if (t_shadow_build) return 0;
     const bool had = m->pcol != nullptr;
     free_packed(m);
     if (had) {   // the SELL kernels' own long-row rule again
@@ -833,6 +838,46 @@ __global__ void k_shadow_maps(const int32_t* __restrict__ sh_order, int64_t sh_r
 
 namespace sellb {
 
+// The cost model's candidates are settled by the clock: whole-matrix SpMVs on
+// a scratch x (zeros) / y, alternately through the caller's layout and through
+// the shadow, one warm-up and three timed launches each way (CUDA events on
+// the build's stream); best of three.  Byte counts alone mislead both ways:
+// cfg3 sigma = 1's packed copy streams ~V_alg yet is latency-bound (the
+// shadow wins 1.45x), cfg4's spikes already sit in the side table and its
+// bulk chunks are full (the shadow's map and scattered stores lose 8 %).
+int time_shadow_choice(sellb_mat* m, cudaStream_t st, float* t_base, float* t_shadow) {
+    const size_t vs = vsize(m->dtype);
+    DBuf x, y;
+    SELLB_CU(x.alloc(std::max<int64_t>(m->n_cols, 1) * vs, st));
+    SELLB_CU(y.alloc(std::max<int64_t>(m->n_pad, 1) * vs, st));
+    SELLB_CU(cudaMemsetAsync(x.p, 0, std::max<int64_t>(m->n_cols, 1) * vs, st));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    SELLB_CU(cudaEventCreate(&e0));
+    if (cudaEventCreate(&e1) != cudaSuccess) { cudaEventDestroy(e0); return set_error(SELLB_ERESOURCE, "event creation failed"); }
+    sellb_mat* sh = m->shadow;
+    float best[2] = {3.0e38f, 3.0e38f};
+    int rc = 0;
+    for (int rep = 0; rep < 4 && !rc; ++rep) {
+        for (int way = 0; way < 2 && !rc; ++way) {
+            m->shadow = way ? sh : nullptr;
+            cudaEventRecord(e0, st);
+            rc = launch_spmv(m, x.p, y.p, 0, m->n_chunks, 0, SELLB_ORDER_STORED, st);
+            cudaEventRecord(e1, st);
+            if (cudaEventSynchronize(e1) != cudaSuccess && !rc)
+                rc = set_error(SELLB_ERESOURCE, "timing the shadow layout failed");
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0) best[way] = std::min(best[way], ms);
+        }
+    }
+    m->shadow = sh;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *t_base = best[0];
+    *t_shadow = best[1];
+    return rc;
+}
+
 void free_shadow(sellb_mat* m) {
     if (m->shadow) {
         free_mat_arrays(m->shadow);
@@ -852,8 +897,7 @@ void free_shadow(sellb_mat* m) {
 // sort scatters rows, and with x in L2 the gathers do not care where a row
 // sits -- else SELL-32-512)
 int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
-    static thread_local bool building = false;
-    if (building) return 0;                       // the shadow's own build
+    if (t_shadow_build) return 0;                 // the shadow's own build
     free_shadow(m);
     bool from_env = false;
     if (force == -2) {
@@ -878,6 +922,7 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
     if (const char* e = getenv("SELLB_SHADOW_X_MAX")) x_max = atof(e);
     const bool x_in_l2 = (double)m->n_cols * (double)vs <= x_max;
     const int64_t sh_sigma = x_in_l2 ? m->n_pad : 512;
+    const bool cost_model = force < 0;
     if (force < 0) {
         const double beta = m->slots ? (double)m->nnz / (double)m->slots : 1.0;
         const bool sorted = m->C == 32 && m->sigma_eff >= std::min<int64_t>(sh_sigma, m->n_pad);
@@ -897,7 +942,8 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
     };
     // 1. the caller's stored rows as a CRS (every row, slot order)
     const int64_t n = m->n_pad;
-    DBuf d_len, d_rpt, d_col, d_val, d_tmp;
+    DBuf d_len, d_rpt, d_tmp;
+    BigBuf d_col, d_val;
     SELLB_CU(d_len.alloc((n + 1) * 8, st));
     SELLB_CU(d_rpt.alloc((n + 1) * 8, st));
     SELLB_CU(cudaMemsetAsync(d_len.p, 0, 8, st));
@@ -909,8 +955,8 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
     SELLB_CU(d_tmp.alloc(tmp_bytes, st));
     SELLB_CU(cub::DeviceScan::InclusiveSum(d_tmp.p, tmp_bytes, d_len.as<int64_t>(),
                                            d_rpt.as<int64_t>(), n + 1, st));
-    SELLB_CU(d_col.alloc(m->nnz * 4, st));
-    SELLB_CU(d_val.alloc(m->nnz * vs, st));
+    SELLB_CU(d_col.alloc(m->nnz * 4));
+    SELLB_CU(d_val.alloc(m->nnz * vs));
     const unsigned grid = (unsigned)grid_for(n * 32, 256);
     if (m->dtype == SELLB_F32)
         k_packed_fill<float><<<grid, 256, 0, st>>>(m->cs, m->rl, m->col, (const float*)m->val, n,
@@ -924,19 +970,17 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
     mark("stored CRS");
     // 2. SELL-32-N of those rows (the device builder: stable sort by length)
     sellb_mat* sh = nullptr;
-    building = true;
+    t_shadow_build = true;
     const int rc_b = sellb_build_from_crs(d_rpt.as<int64_t>(), d_col.as<int32_t>(), d_val.p,
                                           m->dtype, n, m->n_cols, 32, std::min<int64_t>(sh_sigma, n),
                                           1, 0, m->device, st, 1, &sh);
-    building = false;
+    t_shadow_build = false;
     if (rc_b) return rc_b;
     mark("layout");
     m->shadow = sh;
     // the shadow keeps the variant its cost model chose (the pad-inclusive
-    // kernels skip its padding when x[0] is not finite) and never a packed
-    // copy of its own
-    if (sh->pcol)
-        if (int rc = build_packed(sh, st, 0)) { free_shadow(m); return rc; }
+    // kernels skip its padding when x[0] is not finite) and never has a
+    // packed copy of its own (t_shadow_build)
     // 3. output maps
     if (int rc = alloc_dev((void**)&m->sh_ord_st, sh->n_pad * 4)) { free_shadow(m); return rc; }
     if (int rc = alloc_dev((void**)&m->sh_ord_or, sh->n_pad * 4)) { free_shadow(m); return rc; }
@@ -946,6 +990,14 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
     if (int rc = check_stream_error()) { free_shadow(m); return rc; }
     SELLB_CU(cudaStreamSynchronize(st));
     mark("maps");
+    if (cost_model && !(getenv("SELLB_SHADOW_TIME") && !atoi(getenv("SELLB_SHADOW_TIME")))) {
+        float t_base = 0.0f, t_shadow = 0.0f;
+        if (int rc = time_shadow_choice(m, st, &t_base, &t_shadow)) { free_shadow(m); return rc; }
+        if (trace)
+            fprintf(stderr, "shadow timed: as built %.4f ms, shadow %.4f ms\n", t_base, t_shadow);
+        if (!(t_shadow < 0.97f * t_base)) free_shadow(m);    // keep it for a clear win only
+        mark("timed");
+    }
     return 0;
 }
 
@@ -1024,15 +1076,16 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     if (nnz < 0) return set_error(SELLB_ESTRUCT, "rpt[-1] must be >= 0");
     if (nnz && (!col || !val)) return set_error(SELLB_EPARAM, "col/val must not be NULL");
 
-    DBuf d_rpt, d_col, d_val;
+    DBuf d_rpt;
+    BigBuf d_col, d_val;
     const int64_t* rpt_d = rpt;
     const int32_t* col_d = col;
     const void* val_d = val;
     if (!ptrs_on_device) {
         SELLB_CU(d_rpt.alloc((n + 1) * 8, st));
         SELLB_CU(cudaMemcpyAsync(d_rpt.p, rpt, (n + 1) * 8, cudaMemcpyHostToDevice, st));
-        SELLB_CU(d_col.alloc(nnz * 4, st));
-        SELLB_CU(d_val.alloc(nnz * vs, st));
+        SELLB_CU(d_col.alloc(nnz * 4));
+        SELLB_CU(d_val.alloc(nnz * vs));
         if (nnz) {
             SELLB_CU(cudaMemcpyAsync(d_col.p, col, nnz * 4, cudaMemcpyHostToDevice, st));
             SELLB_CU(cudaMemcpyAsync(d_val.p, val, nnz * vs, cudaMemcpyHostToDevice, st));
@@ -1187,23 +1240,19 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     if (int rc = alloc_dev(&m->val, total * vs)) return rc;
     mark("alloc");
     if (n_pad && total) {
-        static const int fill_u = getenv("SELLB_FILL_U") ? atoi(getenv("SELLB_FILL_U")) : 4;
         const unsigned grid = (unsigned)grid_for(n_pad, 256);
         int* const chk = permute_cols ? nullptr : d_bad;
-#define SELLB_FILL(T, U)                                                                       \
-        k_fill<T, U><<<grid, 256, 0, st>>>(rpt_d, col_d, (const T*)val_d, n, n_pad, C, m->order, \
-                                           m->rl, m->cs, m->cl, m->perm, permute_cols ? 1 : 0, \
-                                           m->col, (T*)m->val, n_cols, chk)
-        if (dtype == SELLB_F64) {
-            if (fill_u == 1) SELLB_FILL(double, 1);
-            else if (fill_u == 8) SELLB_FILL(double, 8);
-            else SELLB_FILL(double, 4);
-        } else {
-            if (fill_u == 1) SELLB_FILL(float, 1);
-            else if (fill_u == 8) SELLB_FILL(float, 8);
-            else SELLB_FILL(float, 4);
-        }
-#undef SELLB_FILL
+        // U = 4 (U = 1: same 6.9 ms on cfg5; U = 8: slower)
+        if (dtype == SELLB_F64)
+            k_fill<double, 4><<<grid, 256, 0, st>>>(rpt_d, col_d, (const double*)val_d, n, n_pad, C,
+                                                    m->order, m->rl, m->cs, m->cl, m->perm,
+                                                    permute_cols ? 1 : 0, m->col,
+                                                    (double*)m->val, n_cols, chk);
+        else
+            k_fill<float, 4><<<grid, 256, 0, st>>>(rpt_d, col_d, (const float*)val_d, n, n_pad, C,
+                                                   m->order, m->rl, m->cs, m->cl, m->perm,
+                                                   permute_cols ? 1 : 0, m->col, (float*)m->val,
+                                                   n_cols, chk);
     }
     if (int rc = check_stream_error()) return rc;
     if (nnz && !permute_cols) {

@@ -177,6 +177,19 @@ struct PoolTrim {
     }
 };
 
+// Large build temporaries (GBs): plain cudaMalloc / cudaFree.  Growing the
+// stream-ordered pool by 16 GB cost ~90 ms on the box (cfg5 shadow build)
+// against ~1 ms for cudaMalloc of the same size.
+struct BigBuf {
+    void* p = nullptr;
+    BigBuf() = default;
+    BigBuf(const BigBuf&) = delete;
+    BigBuf& operator=(const BigBuf&) = delete;
+    ~BigBuf() { if (p) cudaFree(p); }
+    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
 // launch helpers implemented in sellb_spmv.cu
 int launch_spmv(const sellb_mat* m, const void* x, void* y, int64_t c0, int64_t c1,
                 int accumulate, int out_order, cudaStream_t st);

@@ -117,9 +117,11 @@ def test_shadow_chunk_ranges_keep_caller_layout():
     assert yd.cpu().numpy().tobytes() == oracle.spmv_sell(o, x).tobytes()
 
 
-def test_shadow_cost_model_choices():
-    """Irregular layouts get the shadow (SELL-32-N with x in L2); dense and
-    already SELL-32-N ones do not."""
+def test_shadow_cost_model_choices(monkeypatch):
+    """The byte-level shortlist (SELLB_SHADOW_TIME=0 skips the timed
+    decision): irregular layouts get the shadow (SELL-32-N with x in L2);
+    dense and already SELL-32-N ones do not."""
+    monkeypatch.setenv("SELLB_SHADOW_TIME", "0")
     pl = generate.powerlaw(200_000, seed=4, band=5000)
     heavy = sb.crs_to_sell(pl, 32, 1)
     heavy8 = sb.crs_to_sell(pl, 8, 1)
@@ -130,10 +132,11 @@ def test_shadow_cost_model_choices():
     assert heavy.shadow and heavy8.shadow and not dense.shadow and not sorted_.shadow
 
 
-def test_shadow_from_host_arrays():
+def test_shadow_from_host_arrays(monkeypatch):
     """A layout uploaded from host arrays (sellb_import, the reference
     dataclass's shape) applies the same cost model and multiplies
     identically."""
+    monkeypatch.setenv("SELLB_SHADOW_TIME", "0")
     m = MATS["powerlaw"]()
     o = oracle.crs_to_sell(m.rpt, m.col, m.val, m.n_rows, m.n_cols, 32, 1)
     s = sb.SellMatrix(o.n_rows, o.n_cols, o.C, o.sigma, o.n_rows_padded, o.n_chunks, o.cs,
@@ -176,6 +179,7 @@ def test_shadow_windowed_for_large_x(monkeypatch, C, sigma):
     neighbours; layouts already sorted over >= 512 rows get none.  Bitwise
     either way."""
     monkeypatch.setenv("SELLB_SHADOW_X_MAX", "0")
+    monkeypatch.setenv("SELLB_SHADOW_TIME", "0")
     m = MATS["powerlaw"]()
     s = sb.crs_to_sell(m, C, sigma)
     assert s.shadow and s.shadow_sigma == 512
@@ -185,3 +189,18 @@ def test_shadow_windowed_for_large_x(monkeypatch, C, sigma):
     monkeypatch.delenv("SELLB_SHADOW_X_MAX")
     s.set_shadow(None)
     assert s.shadow_sigma >= s.n_rows_padded
+
+
+@pytest.mark.parametrize("name", sorted(MATS))
+@pytest.mark.parametrize("C,sigma", [(32, 1), (8, 1), (32, 512)])
+def test_shadow_timed_choice_keeps_results(name, C, sigma):
+    """The default cost model settles its shortlist by timing both layouts at
+    build time; whichever it keeps, y is the oracle's bit for bit (and a
+    re-applied cost model may choose differently without changing y)."""
+    m = MATS[name]()
+    o = oracle.crs_to_sell(m.rpt, m.col, m.val, m.n_rows, m.n_cols, C, sigma)
+    x = generate.rhs(m.n_cols)
+    s = sb.crs_to_sell(m, C, sigma)
+    _check(s, o, x, np.float64)
+    s.set_shadow(None)
+    _check(s, o, x, np.float64)

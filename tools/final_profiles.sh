@@ -17,8 +17,13 @@ run() { name=$1; shift
   rm -f gpurun_out/$T/$name.ncu-rep
   echo "$name done"
 }
-KREGEX="k_spmv_sell"      run cfg2        --config cfg2
-KREGEX="k_spmv_sell"      run cfg3_sN     --config cfg3 --sigma 4000000
-KREGEX="k_spmv_long_grp"  run cfg4_sN_grp --config cfg4 --sigma 2097152
-KREGEX="k_spmv_sell"      run cfg4_sN     --config cfg4 --sigma 2097152
-KREGEX="k_spmv_sell"      run cfg5_s512   --config cfg5 --sigma 512
+# PROFILES="cfg5_s512 cfg3_s1" selects a subset (default: all)
+want() { [ -z "$PROFILES" ] || echo " $PROFILES " | grep -q " $1 "; }
+want cfg5_s512 && KREGEX="k_spmv_sell" run cfg5_s512 --config cfg5 --sigma 512
+want cfg2      && KREGEX="k_spmv_sell" run cfg2      --config cfg2
+want cfg3_sN   && KREGEX="k_spmv_sell" run cfg3_sN   --config cfg3 --sigma 4000000
+# the irregular layouts run through their SELL-32 shadow (ORD 2 epilogue)
+want cfg3_s1   && KREGEX="k_spmv_sell" run cfg3_s1   --config cfg3 --sigma 1
+want cfg3_s512 && KREGEX="k_spmv_sell" run cfg3_s512 --config cfg3 --sigma 512
+want cfg5_s1   && KREGEX="k_spmv_sell" run cfg5_s1   --config cfg5 --sigma 1
+want cfg4_sN   && KREGEX="k_spmv_sell" run cfg4_sN   --config cfg4 --sigma 2097152
