@@ -237,6 +237,70 @@ __global__ void k_fill(const int64_t* __restrict__ rpt, const int32_t* __restric
     if (bad && flag) atomicExch(bad, 2);
 }
 
+// C a multiple of 32 (opt-in A/B, SELLB_FILL_WARP=1): one warp per 32
+// consecutive stored rows of a chunk.  For each 32-slot block the warp issues
+// all 32 rows' loads at once (lanes over a row's entries, coalesced whatever
+// the row lengths; 64 loads in flight per warp), then transposes through a
+// 32 x 32 XOR-swizzled shared tile per array and stores slot by slot (lane =
+// row, coalesced like k_fill).
+template <typename T>
+__global__ void __launch_bounds__(128) k_fill_warp(
+        const int64_t* __restrict__ rpt, const int32_t* __restrict__ col_in,
+        const T* __restrict__ val_in, int64_t n, int64_t n_pad, int64_t C,
+        const int32_t* __restrict__ order, const int32_t* __restrict__ rl,
+        const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
+        const int32_t* __restrict__ perm, int permute_cols, int32_t* __restrict__ col_out,
+        T* __restrict__ val_out, int64_t n_cols, int* __restrict__ bad) {
+    __shared__ T s_val[4][32][32];
+    __shared__ int32_t s_col[4][32][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t n_groups = n_pad >> 5;
+    int flag = 0;
+    for (int64_t g = (int64_t)blockIdx.x * 4 + wib; g < n_groups; g += (int64_t)gridDim.x * 4) {
+        const int64_t p = (g << 5) + lane;
+        const int64_t chunk = (g << 5) / C;
+        const int64_t base = cs[chunk] + ((g << 5) - chunk * C);
+        const int32_t w = cl[chunk];
+        const int32_t len = rl[p];
+        const int32_t o = order[p];
+        const int64_t src = (o < n) ? rpt[o] : 0;
+        for (int32_t jb = 0; jb < w; jb += 32) {
+            const int32_t j = jb + lane;
+            T v[32];
+            int32_t c[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                const int32_t len_r = __shfl_sync(0xffffffffu, len, r);
+                const int64_t src_r = __shfl_sync(0xffffffffu, src, r);
+                v[r] = T(0);
+                c[r] = 0;
+                if (j < len_r) {
+                    v[r] = __ldg(val_in + src_r + j);
+                    c[r] = __ldg(col_in + src_r + j);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                if (j < __shfl_sync(0xffffffffu, len, r)) {
+                    if (bad) flag |= (c[r] < 0) | ((int64_t)c[r] >= n_cols);
+                    if (permute_cols) c[r] = perm[c[r]];
+                }
+                s_val[wib][lane][r ^ lane] = v[r];
+                s_col[wib][lane][r ^ lane] = c[r];
+            }
+            __syncwarp();
+            const int32_t nj = min(32, w - jb);
+            for (int32_t jj = 0; jj < nj; ++jj) {
+                const int64_t d = base + (int64_t)(jb + jj) * C + lane;
+                __stcs(val_out + d, s_val[wib][jj][lane ^ jj]);
+                __stcs(col_out + d, s_col[wib][jj][lane ^ jj]);
+            }
+            __syncwarp();
+        }
+    }
+    if (bad && flag) atomicExch(bad, 2);
+}
+
 // sector accounting for the cost model: a 32-byte sector of val (4 fp64 / 8
 // fp32 lanes) or col (8 lanes) is fetched for slot j iff one of its lanes has
 // j < row length.  Sum over lane groups of the group's max length.
@@ -261,9 +325,18 @@ __global__ void k_sector_count(const int32_t* __restrict__ rl, int64_t n_pad, in
         sv += __shfl_xor_sync(0xffffffffu, sv, o);
         sc += __shfl_xor_sync(0xffffffffu, sc, o);
     }
+    // per block in shared memory, then one pair of global atomics per block
+    __shared__ unsigned long long s_sum[2];
+    if (threadIdx.x == 0) s_sum[0] = s_sum[1] = 0;
+    __syncthreads();
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(out, sv);
-        atomicAdd(out + 1, sc);
+        atomicAdd(&s_sum[0], sv);
+        atomicAdd(&s_sum[1], sc);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd(out, s_sum[0]);
+        atomicAdd(out + 1, s_sum[1]);
     }
 }
 
@@ -360,13 +433,18 @@ int bits_for(uint64_t v) {
 void free_mat_arrays(sellb_mat* m) {
     if (!m) return;
     DeviceGuard g(m->device);
-    cudaFree(m->cs);
-    cudaFree(m->cl);
+    if (m->meta_slab) {
+        cudaFree(m->meta_slab);
+    } else {
+        cudaFree(m->cs);
+        cudaFree(m->cl);
+        cudaFree(m->rl);
+        cudaFree(m->perm);
+        cudaFree(m->order);
+    }
+    m->meta_slab = nullptr;
     cudaFree(m->col);
     cudaFree(m->val);
-    cudaFree(m->rl);
-    cudaFree(m->perm);
-    cudaFree(m->order);
     cudaFree(m->long_rows);
     cudaFree(m->chunk_th);
     cudaFree(m->long_groups);
@@ -839,9 +917,10 @@ __global__ void k_shadow_maps(const int32_t* __restrict__ sh_order, int64_t sh_r
 namespace sellb {
 
 // The cost model's candidates are settled by the clock: whole-matrix SpMVs on
-// a scratch x (zeros) / y, alternately through the caller's layout and through
-// the shadow, one warm-up and three timed launches each way (CUDA events on
-// the build's stream); best of three.  Byte counts alone mislead both ways:
+// a scratch x (zeros) / y, alternately through the caller's layout and
+// through the shadow -- one warm-up round, then five rounds of K back-to-back
+// launches each way (K sized so a round lasts >= ~0.5 ms; CUDA events on the
+// build's stream), best round per way.  Byte counts alone mislead both ways:
 // cfg3 sigma = 1's packed copy streams ~V_alg yet is latency-bound (the
 // shadow wins 1.45x), cfg4's spikes already sit in the side table and its
 // bulk chunks are full (the shadow's map and scattered stores lose 8 %).
@@ -853,21 +932,32 @@ int time_shadow_choice(sellb_mat* m, cudaStream_t st, float* t_base, float* t_sh
     SELLB_CU(cudaMemsetAsync(x.p, 0, std::max<int64_t>(m->n_cols, 1) * vs, st));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     SELLB_CU(cudaEventCreate(&e0));
-    if (cudaEventCreate(&e1) != cudaSuccess) { cudaEventDestroy(e0); return set_error(SELLB_ERESOURCE, "event creation failed"); }
+    if (cudaEventCreate(&e1) != cudaSuccess) {
+        cudaEventDestroy(e0);
+        return set_error(SELLB_ERESOURCE, "event creation failed");
+    }
     sellb_mat* sh = m->shadow;
     float best[2] = {3.0e38f, 3.0e38f};
+    int k_launch = 1;
     int rc = 0;
-    for (int rep = 0; rep < 4 && !rc; ++rep) {
+    for (int rep = 0; rep < 6 && !rc; ++rep) {
         for (int way = 0; way < 2 && !rc; ++way) {
             m->shadow = way ? sh : nullptr;
             cudaEventRecord(e0, st);
-            rc = launch_spmv(m, x.p, y.p, 0, m->n_chunks, 0, SELLB_ORDER_STORED, st);
+            for (int k = 0; k < k_launch && !rc; ++k)
+                rc = launch_spmv(m, x.p, y.p, 0, m->n_chunks, 0, SELLB_ORDER_STORED, st);
             cudaEventRecord(e1, st);
             if (cudaEventSynchronize(e1) != cudaSuccess && !rc)
                 rc = set_error(SELLB_ERESOURCE, "timing the shadow layout failed");
             float ms = 0.0f;
             cudaEventElapsedTime(&ms, e0, e1);
-            if (rep > 0) best[way] = std::min(best[way], ms);
+            if (rep > 0) best[way] = std::min(best[way], ms / (float)k_launch);
+            else best[way] = ms;              // warm-up: one launch each way
+        }
+        if (rep == 0) {   // size the timed rounds from the warm-up launches
+            const float t1 = std::max(std::min(best[0], best[1]), 1e-3f);
+            k_launch = (int)std::min(16.0f, std::max(1.0f, 0.5f / t1));
+            best[0] = best[1] = 3.0e38f;
         }
     }
     m->shadow = sh;
@@ -995,7 +1085,7 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
         if (int rc = time_shadow_choice(m, st, &t_base, &t_shadow)) { free_shadow(m); return rc; }
         if (trace)
             fprintf(stderr, "shadow timed: as built %.4f ms, shadow %.4f ms\n", t_base, t_shadow);
-        if (!(t_shadow < 0.97f * t_base)) free_shadow(m);    // keep it for a clear win only
+        if (!(t_shadow < 0.95f * t_base)) free_shadow(m);    // keep it for a clear win only
         mark("timed");
     }
     return 0;
@@ -1132,11 +1222,20 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     mark("lengths");
 
     // --- 2.-4. scope sort, perm / row_lengths / order, chunk widths ---------
-    if (int rc = alloc_dev((void**)&m->perm, std::max<int64_t>(n, 1) * 4)) return rc;
-    if (int rc = alloc_dev((void**)&m->rl, std::max<int64_t>(n_pad, 1) * 4)) return rc;
-    if (int rc = alloc_dev((void**)&m->order, std::max<int64_t>(n_pad, 1) * 4)) return rc;
-    if (int rc = alloc_dev((void**)&m->cl, std::max<int64_t>(n_chunks, 1) * 4)) return rc;
-    if (int rc = alloc_dev((void**)&m->cs, (n_chunks + 1) * 8)) return rc;
+    {   // one allocation for the five row / chunk arrays (five cudaMalloc calls
+        // of up to 256 MB each cost ~1.5 ms on cfg5)
+        auto up = [](int64_t b) { return (b + 255) / 256 * 256; };
+        const int64_t b_cs = up((n_chunks + 1) * 8), b_cl = up(std::max<int64_t>(n_chunks, 1) * 4);
+        const int64_t b_perm = up(std::max<int64_t>(n, 1) * 4);
+        const int64_t b_row = up(std::max<int64_t>(n_pad, 1) * 4);
+        if (int rc = alloc_dev(&m->meta_slab, b_cs + b_cl + b_perm + 2 * b_row)) return rc;
+        char* q = static_cast<char*>(m->meta_slab);
+        m->cs = reinterpret_cast<int64_t*>(q);
+        m->cl = reinterpret_cast<int32_t*>(q + b_cs);
+        m->perm = reinterpret_cast<int32_t*>(q + b_cs + b_cl);
+        m->rl = reinterpret_cast<int32_t*>(q + b_cs + b_cl + b_perm);
+        m->order = reinterpret_cast<int32_t*>(q + b_cs + b_cl + b_perm + b_row);
+    }
     SELLB_CU(cudaMemsetAsync(m->cs, 0, 8, st));
     int64_t unit = 1;
     if (align_bytes > 1) {
@@ -1243,7 +1342,19 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
         const unsigned grid = (unsigned)grid_for(n_pad, 256);
         int* const chk = permute_cols ? nullptr : d_bad;
         // U = 4 (U = 1: same 6.9 ms on cfg5; U = 8: slower)
-        if (dtype == SELLB_F64)
+        static const bool fill_warp = getenv("SELLB_FILL_WARP") && atoi(getenv("SELLB_FILL_WARP"));
+        const unsigned wgrid = (unsigned)std::min<int64_t>((n_pad / 32 + 3) / 4, 148 * 4);
+        if (fill_warp && C % 32 == 0 && dtype == SELLB_F64)
+            k_fill_warp<double><<<wgrid, 128, 0, st>>>(rpt_d, col_d, (const double*)val_d, n,
+                                                       n_pad, C, m->order, m->rl, m->cs, m->cl,
+                                                       m->perm, permute_cols ? 1 : 0, m->col,
+                                                       (double*)m->val, n_cols, chk);
+        else if (fill_warp && C % 32 == 0)
+            k_fill_warp<float><<<wgrid, 128, 0, st>>>(rpt_d, col_d, (const float*)val_d, n,
+                                                      n_pad, C, m->order, m->rl, m->cs, m->cl,
+                                                      m->perm, permute_cols ? 1 : 0, m->col,
+                                                      (float*)m->val, n_cols, chk);
+        else if (dtype == SELLB_F64)
             k_fill<double, 4><<<grid, 256, 0, st>>>(rpt_d, col_d, (const double*)val_d, n, n_pad, C,
                                                     m->order, m->rl, m->cs, m->cl, m->perm,
                                                     permute_cols ? 1 : 0, m->col,

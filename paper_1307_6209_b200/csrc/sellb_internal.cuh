@@ -87,6 +87,8 @@ struct sellb_mat {
     // the row was shorter than its chunk in the caller's layout (the
     // reference's 0 * x[0] padding term)
     sellb_mat* shadow = nullptr;
+    // cs / cl / perm / row_lengths / order of a device build in one allocation
+    void* meta_slab = nullptr;
     int32_t* sh_ord_st = nullptr;
     int32_t* sh_ord_or = nullptr;
     int32_t long_th = 0x7fffffff;     // chunks wider than this may hold long rows

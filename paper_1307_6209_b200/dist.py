@@ -473,6 +473,8 @@ def setup_device(rpt_t, col_t, val_t, n_global, bounds, C, sigma, rank, world, d
     n_local = rpt_t.numel() - 1
     s = crs_to_sell_device(rpt_t, col_t, val_t, n_local, n_global, C, sigma,
                            device=device.index or 0)
+    if world > 1 and s.shadow:
+        s.set_shadow(False)     # interior / boundary chunk runs keep the block's own layout
     info = s.info()
     has_padding = info.slots > info.nnz
     if gathered is None:
@@ -504,6 +506,8 @@ def cuda_engine_factory(C, sigma, device, dtype=None):
 
     def make(crs_local):
         s = crs_to_sell(crs_local, C, sigma, device=device.index or 0, dtype=dtype)
+        if s.shadow:
+            s.set_shadow(False)  # interior / boundary chunk runs keep the block's own layout
         rl = s.row_lengths
         cl = s.cl
         has_pad = bool(len(rl) and np.any(rl < np.repeat(cl, C)))

@@ -17,6 +17,8 @@ each with cudaProfilerStart/Stop and records how many kernels it launched):
 and without ncu for timing:
     python tools/alpha_sweep.py time gpurun_out/alpha_times.json
 Here (CPU):
+    python tools/alpha_sweep.py traffic gpurun_out/alpha_layouts.json \
+        gpurun_out/alpha.csv profiles/ncu_traffic.json
     python tools/alpha_sweep.py report gpurun_out/alpha_layouts.json \
         gpurun_out/alpha.csv gpurun_out/alpha_times.json > profiles/r01_alpha_sweep.md
 """
@@ -101,6 +103,38 @@ def measure(sb, lib, torch, name, sigma, s, x, y, timed):
     return rec
 
 
+def dram_per_layout(layouts_json, ncu_csv):
+    """[(row, dram bytes of that layout's one SpMV)] from the run's layouts
+    and the ncu CSV (a layout's launches summed)."""
+    rows = json.load(open(layouts_json))
+    lines = open(ncu_csv).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    recs = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    per = {}
+    for r in recs:
+        if r["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            per[r["ID"]] = per.get(r["ID"], 0.0) + float(r["Metric Value"]) * scale[r["Metric Unit"]]
+    ids = sorted(per, key=int)
+    out, k = [], 0
+    for row in rows:
+        n = row.get("launches", 1)
+        out.append((row, sum(per[i] for i in ids[k:k + n])))
+        k += n
+    assert k == len(ids), (k, len(ids))
+    return out
+
+
+def traffic(layouts_json, ncu_csv, traffic_json):
+    """Merge the measured DRAM bytes into profiles/ncu_traffic.json (the keys
+    bench.py reads: <cfg>_s<sigma>_f64[_shadow])."""
+    d = json.load(open(traffic_json))
+    for row, dram in dram_per_layout(layouts_json, ncu_csv):
+        key = f"{row['name']}_s{row['sigma']}_f64" + ("_shadow" if row.get("shadow") else "")
+        d[key] = int(dram)
+    json.dump(d, open(traffic_json, "w"), indent=1)
+
+
 def report(layouts_json, ncu_csv, times_json):
     from paper_1307_6209_b200 import model
     rows = json.load(open(layouts_json))
@@ -177,12 +211,14 @@ def report(layouts_json, ncu_csv, times_json):
                                         extra_bytes=extra)
         v_alg = model.algorithmic_bytes(nnz, row["n_cols"], row["n_pad"], row["n_chunks"])
         bal = model.code_balance_sell(1.0 / nzc, row["beta"], nzr)
-        t = times[(row["name"], row["sigma"], row.get("shadow", False))]
+        # the timed run builds its own layouts; its shadow choice is timed too
+        t = times.get((row["name"], row["sigma"], row.get("shadow", False)))
+        gfs = f"{2 * nnz / t / 1e9:.1f}" if t else "n/a"
         print(f"| {row['name']} | {row['sigma']} | {row['beta']:.4f} | {row['beta_eff']:.4f} | "
               f"{row['variant']} | {dram / 1e6:.1f} | {v_alg / 1e6:.1f} | "
               f"{mat / 1e6:.0f} / {mat64 / 1e6:.0f} | {a_p.alpha:.3f} | "
               f"{a_p.in_range} | {a_e.alpha:.3f} | {a_64.alpha:.3f} | {1 / nzc:.3f} | {bal:.3f} | "
-              f"{2 * nnz / t / 1e9:.1f} | {peak / bal:.1f} |")
+              f"{gfs} | {peak / bal:.1f} |")
 
 
 if __name__ == "__main__":
@@ -190,5 +226,7 @@ if __name__ == "__main__":
         run(sys.argv[2])
     elif sys.argv[1] == "time":
         run(sys.argv[2], timed=True)
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
         report(sys.argv[2], sys.argv[3], sys.argv[4])
