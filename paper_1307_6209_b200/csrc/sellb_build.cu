@@ -237,70 +237,6 @@ __global__ void k_fill(const int64_t* __restrict__ rpt, const int32_t* __restric
     if (bad && flag) atomicExch(bad, 2);
 }
 
-// C a multiple of 32 (opt-in A/B, SELLB_FILL_WARP=1): one warp per 32
-// consecutive stored rows of a chunk.  For each 32-slot block the warp issues
-// all 32 rows' loads at once (lanes over a row's entries, coalesced whatever
-// the row lengths; 64 loads in flight per warp), then transposes through a
-// 32 x 32 XOR-swizzled shared tile per array and stores slot by slot (lane =
-// row, coalesced like k_fill).
-template <typename T>
-__global__ void __launch_bounds__(128) k_fill_warp(
-        const int64_t* __restrict__ rpt, const int32_t* __restrict__ col_in,
-        const T* __restrict__ val_in, int64_t n, int64_t n_pad, int64_t C,
-        const int32_t* __restrict__ order, const int32_t* __restrict__ rl,
-        const int64_t* __restrict__ cs, const int32_t* __restrict__ cl,
-        const int32_t* __restrict__ perm, int permute_cols, int32_t* __restrict__ col_out,
-        T* __restrict__ val_out, int64_t n_cols, int* __restrict__ bad) {
-    __shared__ T s_val[4][32][32];
-    __shared__ int32_t s_col[4][32][32];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t n_groups = n_pad >> 5;
-    int flag = 0;
-    for (int64_t g = (int64_t)blockIdx.x * 4 + wib; g < n_groups; g += (int64_t)gridDim.x * 4) {
-        const int64_t p = (g << 5) + lane;
-        const int64_t chunk = (g << 5) / C;
-        const int64_t base = cs[chunk] + ((g << 5) - chunk * C);
-        const int32_t w = cl[chunk];
-        const int32_t len = rl[p];
-        const int32_t o = order[p];
-        const int64_t src = (o < n) ? rpt[o] : 0;
-        for (int32_t jb = 0; jb < w; jb += 32) {
-            const int32_t j = jb + lane;
-            T v[32];
-            int32_t c[32];
-#pragma unroll
-            for (int r = 0; r < 32; ++r) {
-                const int32_t len_r = __shfl_sync(0xffffffffu, len, r);
-                const int64_t src_r = __shfl_sync(0xffffffffu, src, r);
-                v[r] = T(0);
-                c[r] = 0;
-                if (j < len_r) {
-                    v[r] = __ldg(val_in + src_r + j);
-                    c[r] = __ldg(col_in + src_r + j);
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < 32; ++r) {
-                if (j < __shfl_sync(0xffffffffu, len, r)) {
-                    if (bad) flag |= (c[r] < 0) | ((int64_t)c[r] >= n_cols);
-                    if (permute_cols) c[r] = perm[c[r]];
-                }
-                s_val[wib][lane][r ^ lane] = v[r];
-                s_col[wib][lane][r ^ lane] = c[r];
-            }
-            __syncwarp();
-            const int32_t nj = min(32, w - jb);
-            for (int32_t jj = 0; jj < nj; ++jj) {
-                const int64_t d = base + (int64_t)(jb + jj) * C + lane;
-                __stcs(val_out + d, s_val[wib][jj][lane ^ jj]);
-                __stcs(col_out + d, s_col[wib][jj][lane ^ jj]);
-            }
-            __syncwarp();
-        }
-    }
-    if (bad && flag) atomicExch(bad, 2);
-}
-
 // sector accounting for the cost model: a 32-byte sector of val (4 fp64 / 8
 // fp32 lanes) or col (8 lanes) is fetched for slot j iff one of its lanes has
 // j < row length.  Sum over lane groups of the group's max length.
@@ -1341,20 +1277,10 @@ int sellb_build_from_crs(const int64_t* rpt, const int32_t* col, const void* val
     if (n_pad && total) {
         const unsigned grid = (unsigned)grid_for(n_pad, 256);
         int* const chk = permute_cols ? nullptr : d_bad;
-        // U = 4 (U = 1: same 6.9 ms on cfg5; U = 8: slower)
-        static const bool fill_warp = getenv("SELLB_FILL_WARP") && atoi(getenv("SELLB_FILL_WARP"));
-        const unsigned wgrid = (unsigned)std::min<int64_t>((n_pad / 32 + 3) / 4, 148 * 4);
-        if (fill_warp && C % 32 == 0 && dtype == SELLB_F64)
-            k_fill_warp<double><<<wgrid, 128, 0, st>>>(rpt_d, col_d, (const double*)val_d, n,
-                                                       n_pad, C, m->order, m->rl, m->cs, m->cl,
-                                                       m->perm, permute_cols ? 1 : 0, m->col,
-                                                       (double*)m->val, n_cols, chk);
-        else if (fill_warp && C % 32 == 0)
-            k_fill_warp<float><<<wgrid, 128, 0, st>>>(rpt_d, col_d, (const float*)val_d, n,
-                                                      n_pad, C, m->order, m->rl, m->cs, m->cl,
-                                                      m->perm, permute_cols ? 1 : 0, m->col,
-                                                      (float*)m->val, n_cols, chk);
-        else if (dtype == SELLB_F64)
+        // U = 4 (U = 1: same 6.9 ms on cfg5; U = 8 slower; a warp-per-32-rows
+        // transpose through shared memory: 19.7 ms, too few loads in flight).
+        // cfg5: 33.3 GB of DRAM traffic (= the algorithmic bytes) in 6.55 ms
+        if (dtype == SELLB_F64)
             k_fill<double, 4><<<grid, 256, 0, st>>>(rpt_d, col_d, (const double*)val_d, n, n_pad, C,
                                                     m->order, m->rl, m->cs, m->cl, m->perm,
                                                     permute_cols ? 1 : 0, m->col,
