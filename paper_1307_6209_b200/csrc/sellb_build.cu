@@ -918,8 +918,8 @@ void free_shadow(sellb_mat* m) {
 
 // force: 1 build, 0 drop, -1 cost model, -2 the build's default (the cost
 // model unless SELLB_SHADOW says 0 / 1).  Cost model: build when the layout is
-// irregular (chunk occupancy beta < 0.9) and not already sorted as widely as
-// the shadow would be (SELL-32-N when x fits the L2 comfortably -- the global
+// irregular (chunk occupancy beta < 0.9) or C != 32, and not already a C = 32
+// layout sorted as widely as the shadow would be (SELL-32-N when x fits the L2 comfortably -- the global
 // sort scatters rows, and with x in L2 the gathers do not care where a row
 // sits -- else SELL-32-512)
 int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
@@ -952,7 +952,11 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
     if (force < 0) {
         const double beta = m->slots ? (double)m->nnz / (double)m->slots : 1.0;
         const bool sorted = m->C == 32 && m->sigma_eff >= std::min<int64_t>(sh_sigma, m->n_pad);
-        if (sorted || beta >= 0.9) return 0;
+        // C != 32 layouts are candidates whatever their occupancy: the shadow
+        // runs them through the C = 32 kernels (one warp per chunk), which
+        // the generic-C instances trail (cfg4 sigma = N: C = 8 / 128 at
+        // 0.76 / 0.79 of the roofline vs 0.87 for C = 32)
+        if (sorted || (beta >= 0.9 && m->C == 32)) return 0;
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
         if (2.0 * (double)m->nnz * (double)(vs + 4) > 0.5 * (double)free_b) return 0;
@@ -994,36 +998,86 @@ int build_shadow(sellb_mat* m, cudaStream_t st, int force) {
                                                    d_col.as<int32_t>(), d_val.as<double>());
     if (int rc = check_stream_error()) return rc;
     mark("stored CRS");
-    // 2. SELL-32-N of those rows (the device builder: stable sort by length)
-    sellb_mat* sh = nullptr;
-    t_shadow_build = true;
-    const int rc_b = sellb_build_from_crs(d_rpt.as<int64_t>(), d_col.as<int32_t>(), d_val.p,
-                                          m->dtype, n, m->n_cols, 32, std::min<int64_t>(sh_sigma, n),
-                                          1, 0, m->device, st, 1, &sh);
-    t_shadow_build = false;
-    if (rc_b) return rc_b;
-    mark("layout");
-    m->shadow = sh;
-    // the shadow keeps the variant its cost model chose (the pad-inclusive
-    // kernels skip its padding when x[0] is not finite) and never has a
-    // packed copy of its own (t_shadow_build)
-    // 3. output maps
-    if (int rc = alloc_dev((void**)&m->sh_ord_st, sh->n_pad * 4)) { free_shadow(m); return rc; }
-    if (int rc = alloc_dev((void**)&m->sh_ord_or, sh->n_pad * 4)) { free_shadow(m); return rc; }
-    k_shadow_maps<<<(unsigned)grid_for(sh->n_pad, 256), 256, 0, st>>>(
-        sh->order, sh->n_rows, sh->n_pad, m->rl, m->cl, m->C, m->order, m->n_rows, m->n_pad,
-        m->sh_ord_st, m->sh_ord_or);
-    if (int rc = check_stream_error()) { free_shadow(m); return rc; }
-    SELLB_CU(cudaStreamSynchronize(st));
-    mark("maps");
-    if (cost_model && !(getenv("SELLB_SHADOW_TIME") && !atoi(getenv("SELLB_SHADOW_TIME")))) {
+    // 2. candidate layouts of those rows (the device builder), each with its
+    // output maps.  SELL-32 at sh_sigma first; for C != 32 callers also
+    // SELL-32-1 of the stored order (their own rows in C = 32 chunks: what
+    // the C = 32 kernels run best when sorting does not pay, cfg4)
+    struct Cand {
+        sellb_mat* sh = nullptr;
+        int32_t* ord_st = nullptr;
+        int32_t* ord_or = nullptr;
+        float t = 3.0e38f;
+    };
+    auto free_cand = [](Cand& c) {
+        if (c.sh) { free_mat_arrays(c.sh); delete c.sh; }
+        cudaFree(c.ord_st);
+        cudaFree(c.ord_or);
+        c = Cand();
+    };
+    auto build_cand = [&](int64_t sig, Cand& c) -> int {
+        t_shadow_build = true;
+        const int rc_b = sellb_build_from_crs(d_rpt.as<int64_t>(), d_col.as<int32_t>(), d_val.p,
+                                              m->dtype, n, m->n_cols, 32,
+                                              std::min<int64_t>(sig, n), 1, 0, m->device, st, 1,
+                                              &c.sh);
+        t_shadow_build = false;
+        if (rc_b) return rc_b;
+        // the shadow keeps the variant its cost model chose (the pad-inclusive
+        // kernels skip its padding when x[0] is not finite) and never has a
+        // packed copy of its own (t_shadow_build)
+        sellb_mat* sh = c.sh;
+        if (int rc = alloc_dev((void**)&c.ord_st, sh->n_pad * 4)) { free_cand(c); return rc; }
+        if (int rc = alloc_dev((void**)&c.ord_or, sh->n_pad * 4)) { free_cand(c); return rc; }
+        k_shadow_maps<<<(unsigned)grid_for(sh->n_pad, 256), 256, 0, st>>>(
+            sh->order, sh->n_rows, sh->n_pad, m->rl, m->cl, m->C, m->order, m->n_rows, m->n_pad,
+            c.ord_st, c.ord_or);
+        if (int rc = check_stream_error()) { free_cand(c); return rc; }
+        SELLB_CU(cudaStreamSynchronize(st));
+        return 0;
+    };
+    auto install = [&](Cand& c) {
+        m->shadow = c.sh;
+        m->sh_ord_st = c.ord_st;
+        m->sh_ord_or = c.ord_or;
+    };
+    auto uninstall = [&]() {
+        m->shadow = nullptr;
+        m->sh_ord_st = nullptr;
+        m->sh_ord_or = nullptr;
+    };
+    const bool timed = cost_model &&
+                       !(getenv("SELLB_SHADOW_TIME") && !atoi(getenv("SELLB_SHADOW_TIME")));
+    std::vector<int64_t> sigmas{sh_sigma};
+    if (timed && m->C != 32) sigmas.push_back(1);
+    Cand best;
+    for (size_t i = 0; i < sigmas.size(); ++i) {
+        if (i > 0) {   // room for one more copy of the entries next to the kept one
+            size_t free_b = 0, total_b = 0;
+            if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+            if ((double)m->nnz * (double)(vs + 4) > 0.5 * (double)free_b) break;
+        }
+        Cand c;
+        if (int rc = build_cand(sigmas[i], c)) { free_cand(best); return rc; }
+        mark("layout+maps");
+        if (!timed) { install(c); return 0; }
+        install(c);
         float t_base = 0.0f, t_shadow = 0.0f;
-        if (int rc = time_shadow_choice(m, st, &t_base, &t_shadow)) { free_shadow(m); return rc; }
+        const int rc_t = time_shadow_choice(m, st, &t_base, &t_shadow);
+        uninstall();
+        if (rc_t) { free_cand(c); free_cand(best); return rc_t; }
         if (trace)
-            fprintf(stderr, "shadow timed: as built %.4f ms, shadow %.4f ms\n", t_base, t_shadow);
-        if (!(t_shadow < 0.95f * t_base)) free_shadow(m);    // keep it for a clear win only
+            fprintf(stderr, "shadow timed: as built %.4f ms, SELL-32-%lld shadow %.4f ms\n",
+                    t_base, (long long)std::min<int64_t>(sigmas[i], n), t_shadow);
         mark("timed");
+        c.t = t_shadow;
+        if (t_shadow < 0.95f * t_base && t_shadow < best.t) {   // a clear win only
+            free_cand(best);
+            best = c;
+        } else {
+            free_cand(c);
+        }
     }
+    if (best.sh) install(best);
     return 0;
 }
 
