@@ -165,18 +165,23 @@ int sellb_set_variant(sellb_mat* m, int32_t variant);
  * Every build applies the cost model unless SELLB_PACKED=0 / 1 forces it. */
 int sellb_set_packed(sellb_mat* m, int32_t mode);
 
-/* Shadow execution layout for irregular layouts: 1 builds it (a device copy
+/* Shadow execution layout for irregular or C != 32 layouts: 1 builds it (a device copy
  * of the stored rows re-laid as SELL-32-N -- sorted by length over the
  * whole matrix -- when x is at most SELLB_SHADOW_X_MAX bytes (default
  * 48 MiB, i.e. x stays in L2), else as SELL-32-512, which keeps a chunk's
  * rows neighbours and their x lines shared; every full-range sellb_spmv then
  * runs on it and scatters each row's sum to the caller's stored / original
  * row, bit-identical, including the 0 * x[0] term of the caller's padding),
- * 0 drops it, -1 applies the cost model (chunk occupancy < 0.9 and the
- * caller's layout not already sorted that widely).  Every build applies the
- * cost model unless SELLB_SHADOW=0 / 1 forces it.  Chunk-range calls (c0, c1
- * not the whole matrix) keep the caller's layout.  sellb_info_t.shadow is
- * the shadow's sigma (0: none). */
+ * 0 drops it, -1 applies the cost model (chunk occupancy < 0.9 or C != 32,
+ * and the caller's layout not already a C = 32 one sorted that widely; for
+ * C != 32 a SELL-32-1 re-chunking of the stored order is a second
+ * candidate; the fastest timed candidate is kept for a >= 5 % win).  Every
+ * build applies the cost model unless SELLB_SHADOW=0 / 1 forces it.
+ * Chunk-range calls (c0, c1 not the whole matrix) keep the caller's layout.  sellb_info_t.shadow is
+ * the shadow's sigma (0: none).  The cost model times its candidates with
+ * whole-matrix SpMVs on scratch vectors (SELLB_SHADOW_TIME=0 skips that);
+ * like sellb_set_packed / sellb_set_variant it must not run concurrently
+ * with other calls on the same matrix. */
 int sellb_set_shadow(sellb_mat* m, int32_t mode);
 void sellb_free(sellb_mat* m);
 
