@@ -66,6 +66,16 @@ def _sell_handle(cs, cl, C, col, val, n_cols):
         _lib.SELLB_F64, n_chunks * int(C), int(n_cols), int(C), 1, n_chunks, len(val), 0,
         0, None, 0, ctypes.byref(out)))
     h = out.value
+    # the protocol passes no row_lengths: infer them from each row's trailing
+    # (0.0, column 0) slots -- the .sell reader's rule (io.py) -- so the
+    # pad-skipping kernels, long-row roles and shadow layout apply.  Bitwise
+    # the same y: a real trailing (0.0, col 0) entry adds 0*x[0], which the
+    # pad term adds once instead (a no-op for finite x[0], NaN otherwise).
+    try:
+        _lib.check(lib.sellb_infer_row_lengths(h, None))
+    except Exception:
+        _free(h)
+        raise
     try:
         weakref.finalize(val.base if val.base is not None else val, _evict, key)
     except TypeError:
