@@ -67,3 +67,39 @@ def test_scope_sort_all_empty_rows():
         o = oracle.crs_to_sell(m.rpt, m.col, m.val, m.n_rows, m.n_cols, 32, sigma)
         for k in ARRAYS:
             assert getattr(s, k).tobytes() == getattr(o, k).tobytes(), (sigma, k)
+
+
+@pytest.mark.parametrize("bad", [-1, 6000, 2 ** 31 - 1])
+@pytest.mark.parametrize("permute", [False, True])
+def test_device_build_rejects_bad_columns(bad, permute):
+    """Device-input builds (crs_to_sell_device: no host-side validation) check
+    every column -- inside the fill, or before it when columns are permuted
+    -- and raise the reference's StructuralError; the library keeps working."""
+    import torch
+    m = tie_heavy(6000, 6000, seed=11)
+    col = m.col.copy()
+    col[len(col) // 2] = bad
+    dev = torch.device("cuda", 0)
+    rpt_t = torch.from_numpy(m.rpt).to(dev)
+    col_t = torch.from_numpy(col).to(dev)
+    val_t = torch.from_numpy(m.val).to(dev)
+    with pytest.raises(sb.StructuralError, match="column index out of bounds"):
+        sb.crs_to_sell_device(rpt_t, col_t, val_t, m.n_rows, m.n_cols, 32, 512,
+                              permute_cols=permute)
+    good = sb.crs_to_sell_device(rpt_t, torch.from_numpy(m.col).to(dev), val_t, m.n_rows,
+                                 m.n_cols, 32, 512, permute_cols=permute)
+    o = oracle.crs_to_sell(m.rpt, m.col, m.val, m.n_rows, m.n_cols, 32, 512,
+                           permute_cols=permute)
+    for k in ARRAYS:
+        assert getattr(good, k).tobytes() == getattr(o, k).tobytes(), k
+
+
+def test_device_build_rejects_decreasing_rpt():
+    import torch
+    m = tie_heavy(3000, 500, seed=12)
+    rpt = m.rpt.copy()
+    rpt[100] = rpt[101] + 1
+    dev = torch.device("cuda", 0)
+    with pytest.raises(sb.StructuralError, match="non-decreasing"):
+        sb.crs_to_sell_device(torch.from_numpy(rpt).to(dev), torch.from_numpy(m.col).to(dev),
+                              torch.from_numpy(m.val).to(dev), m.n_rows, m.n_cols, 32, 1)
